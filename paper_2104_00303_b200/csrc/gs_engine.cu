@@ -1,0 +1,856 @@
+// gridshift-b200: host orchestration and C ABI (see include/gridshift_cuda.h).
+//
+// One gs_ctx = one device, one stream, a set of grow-only device buffers and
+// pinned host mirrors of the loop-control block.  The iteration loop is
+// device-driven: kernels test Ctrl::done, so the host enqueues iterations in
+// chunks and only synchronises between chunks (no per-iteration round trip).
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gridshift_cuda.h"
+#include "gs_kernels.cuh"
+#include "gs_track.cuh"
+
+using namespace gs;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+  g_err = msg;
+  throw Fail{code};
+}
+
+#define GS_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      fail(GS_ERUNTIME, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                            __FILE__ + ":" + std::to_string(__LINE__) + " (" #call ")"); \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace
+
+struct gs_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t own = nullptr;
+  cudaStream_t st = nullptr;      // stream of the current call
+  std::mutex mu;
+  // device buffers
+  Buf x_stage, y[2], ent[2], keys[2], list[2], targets, partials, par, first, aux, roots,
+      root_first, ranks, modes, labels, mv_hist, fp_hist, k_hist, stats, ctrl, perm, track,
+      track_out, bitmaps;
+  // pinned host mirrors
+  Ctrl* h_ctrl = nullptr;
+  InitStats* h_stats = nullptr;
+  u32* h_small = nullptr;        // pinned scratch for small device->host reads
+  // last-run results
+  int d_last = 0;
+  int64_t k_last = 0;
+  std::vector<double> modes_host;
+  std::vector<int64_t> iter_k;
+  std::vector<uint64_t> iter_fp;
+  std::vector<int64_t> track_bins;
+};
+
+namespace {
+
+template <typename T>
+T* ensure(gs_ctx* c, Buf& b, size_t count, int fill = 0) {
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  if (b.cap < bytes) {
+    if (b.p) GS_CUDA(cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+    const size_t alloc = bytes + bytes / 8;
+    GS_CUDA(cudaMalloc(&b.p, alloc));
+    GS_CUDA(cudaMemsetAsync(b.p, fill, alloc, c->st));
+    b.cap = alloc;
+  }
+  return static_cast<T*>(b.p);
+}
+
+inline int blocks_for(gs_ctx* c, int64_t work, int per_sm = 8) {
+  const int64_t want = (work + kThreads - 1) / kThreads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->sms * per_sm));
+}
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(GS_ERUNTIME, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+}
+
+void sync(gs_ctx* c) { GS_CUDA(cudaStreamSynchronize(c->st)); }
+
+void validate_common(int64_t n, int32_t d, double h) {
+  if (!(std::isfinite(h) && h > 0.0)) {
+    char b[128];
+    snprintf(b, sizeof b, "bandwidth must be a positive finite real, got %.17g", h);
+    fail(GS_EINVAL, b);
+  }
+  if (n < 1 || d < 1) fail(GS_EINVAL, "need n >= 1 and d >= 1");
+  if (d > GS_MAXD) fail(GS_EUNSUPPORTED, "the CUDA engine supports d <= 8 feature axes");
+  if (n >= (int64_t)UINT32_MAX) fail(GS_EUNSUPPORTED, "the CUDA engine supports n < 2^32 points per device");
+}
+
+// Lattice geometry + quantisation from the initial statistics.
+struct Plan {
+  GridParams g;
+  bool dense;
+  uint64_t slots;     // table slots (dense: nkeys, hash: capacity)
+  uint64_t list_cap;  // max occupied cells
+};
+
+Plan make_plan(int64_t n, int d, double h, const InitStats& s) {
+  if (s.flags & kErrNonFinite) fail(GS_EINVAL, "point data contains NaN or infinite entries");
+  if (s.flags & kErrLattice)
+    fail(GS_EINVAL,
+         "cell coordinates exceed the supported integer lattice; bandwidth is too small for this "
+         "coordinate range");
+  Plan p{};
+  GridParams& g = p.g;
+  memset(&g, 0, sizeof g);
+  g.h = h;
+  g.d = d;
+  __int128 prod = 1;
+  double span2 = 0.0;
+  int64_t ext[GS_MAXD];
+  for (int j = 0; j < d; ++j) {
+    // admissible box: observed cells +/- 1 (rounding drift margin), plus a
+    // one-cell neighbour pad on each side for the key origin (grid.py:146-147)
+    g.lo[j] = s.cmin[j] - 1;
+    g.hi[j] = s.cmax[j] + 1;
+    g.base[j] = g.lo[j] - 1;
+    ext[j] = g.hi[j] - g.lo[j] + 3;
+    prod *= ext[j];
+    if (prod >= ((__int128)1 << 62))
+      fail(GS_EUNSUPPORTED,
+           "lattice box exceeds 2^62 cells; the CUDA engine needs packed int64 cell keys");
+    double m;
+    memcpy(&m, &s.absmax[j], sizeof m);
+    int e = 0;
+    if (m > 0) frexp(m, &e);  // m < 2^e
+    int sh = 62 - (e + 1);     // |v| < 2^61
+    sh = std::max(-1000, std::min(1000, sh));
+    g.qexp[j] = sh;
+    g.qscale[j] = ldexp(1.0, sh);
+    const double w = (double)ext[j] * h;
+    span2 += w * w;
+  }
+  uint64_t acc = 1;
+  for (int j = d - 1; j >= 0; --j) {
+    g.stride[j] = acc;
+    acc *= (uint64_t)ext[j];
+  }
+  g.nkeys = acc;
+  int em = 0;
+  frexp(std::sqrt(span2) * 1.0000001 + 1e-300, &em);
+  g.movement_exp = em;
+  const size_t entry = 8 * (1 + 2 * (size_t)d);
+  const uint64_t occ_bound = std::min<uint64_t>((uint64_t)n, g.nkeys);
+  p.dense = g.nkeys <= (1ull << 31) && g.nkeys * entry <= (4ull << 30) &&
+            g.nkeys <= 64ull * (uint64_t)n + (1ull << 22);
+  if (p.dense) {
+    p.slots = g.nkeys;
+    g.mask = 0;
+  } else {
+    uint64_t cap = 256;
+    while (cap < 2 * occ_bound) cap <<= 1;
+    if (cap > (1ull << 31)) fail(GS_EUNSUPPORTED, "hash table would exceed 2^31 slots");
+    p.slots = cap;
+    g.mask = cap - 1;
+  }
+  p.list_cap = occ_bound;
+  return p;
+}
+
+template <int D>
+struct Tabs {
+  DenseTable<D> dn[2];
+  HashTable<D> hs[2];
+};
+
+template <int D>
+Tabs<D> make_tabs(gs_ctx* c, const Plan& p) {
+  Tabs<D> t{};
+  Ctrl* dctrl = static_cast<Ctrl*>(c->ctrl.p);
+  for (int b = 0; b < 2; ++b) {
+    Entry<D>* ent = ensure<Entry<D>>(c, c->ent[b], p.slots, 0);
+    u32* list = ensure<u32>(c, c->list[b], p.list_cap);
+    t.dn[b].ent = ent;
+    t.dn[b].list = list;
+    t.dn[b].k = &dctrl->k[b];
+    t.hs[b].ent = ent;
+    t.hs[b].list = list;
+    t.hs[b].k = &dctrl->k[b];
+    if (!p.dense) {
+      t.hs[b].keys = ensure<u64>(c, c->keys[b], p.slots, 0xff);
+      t.hs[b].mask = p.g.mask;
+    }
+  }
+  return t;
+}
+
+void reset_ctrl(gs_ctx* c) {
+  memset(c->h_ctrl, 0, sizeof(Ctrl));
+  GS_CUDA(cudaMemcpyAsync(c->ctrl.p, c->h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, c->st));
+}
+
+void read_ctrl(gs_ctx* c) {
+  GS_CUDA(cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+}
+
+void check_flags(int flags) {
+  if (flags & kErrOutOfBox) fail(GS_ERUNTIME, "an iterate left the admissible lattice box");
+  if (flags & kErrTableFull) fail(GS_ERUNTIME, "cell hash table overflow");
+  if (flags & kErrMissing) fail(GS_ERUNTIME, "cell lookup missed an occupied cell");
+}
+
+// ------------------------------------------------------------ input stage
+
+enum InKind { IN_F64 = 0, IN_F32 = 1, IN_IMAGE = 2 };
+
+struct Input {
+  InKind kind;
+  const void* dev;    // device pointer
+  int width = 0;      // image
+  double scale = 0;   // image rgbxy scale
+};
+
+template <int D>
+InitStats run_init(gs_ctx* c, const Input& in, int64_t n, double h, double* y0) {
+  InitStats* dst = ensure<InitStats>(c, c->stats, 1);
+  InitStats hs;
+  memset(&hs, 0, sizeof hs);
+  for (int j = 0; j < GS_MAXD; ++j) {
+    hs.cmin[j] = LLONG_MAX;
+    hs.cmax[j] = LLONG_MIN;
+  }
+  *c->h_stats = hs;
+  GS_CUDA(cudaMemcpyAsync(dst, c->h_stats, sizeof hs, cudaMemcpyHostToDevice, c->st));
+  const int nb = blocks_for(c, n);
+  if (in.kind == IN_F64)
+    k_init_aos<D, double><<<nb, kThreads, 0, c->st>>>((const double*)in.dev, y0, n, h, dst);
+  else if (in.kind == IN_F32)
+    k_init_aos<D, float><<<nb, kThreads, 0, c->st>>>((const float*)in.dev, y0, n, h, dst);
+  else {
+    if constexpr (D == 3 || D == 5)
+      k_init_image<D><<<nb, kThreads, 0, c->st>>>((const unsigned char*)in.dev, y0, n, in.width, in.scale, h, dst);
+  }
+  check_launch();
+  GS_CUDA(cudaMemcpyAsync(c->h_stats, dst, sizeof hs, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  return *c->h_stats;
+}
+
+// -------------------------------------------------------------- iteration
+
+template <int D, class Tab>
+void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, int64_t n, int nb_pts,
+                       int nb_cells) {
+  const int cur = t & 1;
+  double* y_in = static_cast<double*>(c->y[cur].p);
+  double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, n, p.g, tabs[cur], ctrl, 1);
+  k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1],
+                                                  static_cast<double*>(c->targets.p), ctrl, cur,
+                                                  static_cast<u64*>(c->fp_hist.p) + t,
+                                                  static_cast<u32*>(c->k_hist.p) + t);
+  k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur],
+                                                  static_cast<const double*>(c->targets.p), ctrl,
+                                                  static_cast<u64*>(c->partials.p),
+                                                  static_cast<double*>(c->mv_hist.p), t, eta, cur);
+}
+
+// Extraction of y_final (modeseek.py:256-272).  Table buffer e is clean on
+// entry, buffer e^1 is dirty (cleared here and used as component scratch).
+template <int D, class Tab>
+void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
+                 int64_t* labels_dev) {
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  const int nb_pts = blocks_for(c, n);
+  const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
+  k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e ^ 1], &ctrl->k[e ^ 1]);
+  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e ^ 1]);
+  k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], ctrl, 0);
+  u32* par = ensure<u32>(c, c->par, p.slots);
+  u32* first = ensure<u32>(c, c->first, p.slots);
+  u32* rankmap = ensure<u32>(c, c->aux, p.slots);
+  u32* roots = ensure<u32>(c, c->roots, p.list_cap + 1);
+  u32* rfirst = ensure<u32>(c, c->root_first, p.list_cap + 1);
+  u32* nroots = ensure<u32>(c, c->partials, 2 * (size_t)c->sms * 8 + 2);  // reuse scratch
+  k_uf_init<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first);
+  k_uf_link<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[e], &ctrl->k[e], par);
+  k_uf_flatten<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, tabs[e ^ 1].ent);
+  k_first<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, first, nullptr, ctrl);
+  GS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(u32), c->st));
+  k_roots<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first, roots, rfirst, nroots);
+  check_launch();
+  u32 nr = 0;
+  GS_CUDA(cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->st));
+  GS_CUDA(cudaMemcpyAsync(c->h_small, nroots, sizeof(u32), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  check_flags(c->h_ctrl->error);
+  nr = c->h_small[0];
+  // dense relabel by first appearance (modeseek.py:262-265): sort roots by
+  // their minimum point index; nr is the number of clusters (small)
+  std::vector<u32> hr(nr), hf(nr);
+  GS_CUDA(cudaMemcpyAsync(hr.data(), roots, nr * sizeof(u32), cudaMemcpyDeviceToHost, c->st));
+  GS_CUDA(cudaMemcpyAsync(hf.data(), rfirst, nr * sizeof(u32), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  std::vector<u32> order(nr);
+  for (u32 i = 0; i < nr; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](u32 a, u32 b) { return hf[a] < hf[b]; });
+  std::vector<u32> rk(nr);
+  for (u32 i = 0; i < nr; ++i) rk[order[i]] = i;
+  u32* dranks = ensure<u32>(c, c->ranks, nr + 1);
+  GS_CUDA(cudaMemcpyAsync(dranks, rk.data(), nr * sizeof(u32), cudaMemcpyHostToDevice, c->st));
+  double* dmodes = ensure<double>(c, c->modes, (size_t)nr * D + 1);
+  k_modes<D><<<blocks_for(c, nr), kThreads, 0, c->st>>>(p.g, roots, dranks, nr, rankmap, tabs[e ^ 1].ent, dmodes);
+  k_labels<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, rankmap, nullptr,
+                                                   reinterpret_cast<i64*>(labels_dev));
+  k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e]);
+  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e]);
+  check_launch();
+  c->modes_host.resize((size_t)nr * D);
+  GS_CUDA(cudaMemcpyAsync(c->modes_host.data(), dmodes, (size_t)nr * D * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  c->k_last = nr;
+  c->d_last = D;
+}
+
+struct RunOut {
+  int64_t k = 0;
+  int iters = 0;
+  int converged = 0;
+};
+
+template <int D>
+RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta, int max_iters,
+                    int64_t* labels_dev, double* movement_out) {
+  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
+  ensure<double>(c, c->y[1], (size_t)n * D);
+  ensure<Ctrl>(c, c->ctrl, 1);
+  const InitStats s = run_init<D>(c, in, n, h, y0);
+  Plan p = make_plan(n, D, h, s);
+  Tabs<D> tabs = make_tabs<D>(c, p);
+  ensure<double>(c, c->targets, p.slots * D);
+  const int nb_pts = blocks_for(c, n);
+  const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
+  ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
+  ensure<double>(c, c->mv_hist, (size_t)max_iters);
+  u64* fp = ensure<u64>(c, c->fp_hist, (size_t)max_iters);
+  ensure<u32>(c, c->k_hist, (size_t)max_iters);
+  GS_CUDA(cudaMemsetAsync(fp, 0, sizeof(u64) * max_iters, c->st));
+  reset_ctrl(c);
+  // device-driven loop: enqueue chunks, synchronise between chunks only
+  int t = 0, chunk = 4;
+  while (t < max_iters) {
+    const int m = std::min(chunk, max_iters - t);
+    for (int q = 0; q < m; ++q, ++t) {
+      if (p.dense)
+        enqueue_iteration<D>(c, p, tabs.dn, t, eta, n, nb_pts, nb_cells);
+      else
+        enqueue_iteration<D>(c, p, tabs.hs, t, eta, n, nb_pts, nb_cells);
+    }
+    check_launch();
+    read_ctrl(c);
+    check_flags(c->h_ctrl->error);
+    if (c->h_ctrl->done) break;
+    chunk = std::min(chunk * 2, 32);
+  }
+  RunOut r;
+  r.iters = c->h_ctrl->iters;
+  r.converged = c->h_ctrl->done;
+  const int e = r.iters & 1;
+  const double* yf = static_cast<const double*>(c->y[e].p);
+  if (p.dense)
+    run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev);
+  else
+    run_extract<D>(c, p, tabs.hs, yf, n, e, labels_dev);
+  r.k = c->k_last;
+  if (movement_out)
+    GS_CUDA(cudaMemcpyAsync(movement_out, c->mv_hist.p, sizeof(double) * r.iters, cudaMemcpyDeviceToHost, c->st));
+  c->iter_k.assign(r.iters, 0);
+  c->iter_fp.assign(r.iters, 0);
+  std::vector<u32> kk(r.iters + 1);
+  GS_CUDA(cudaMemcpyAsync(kk.data(), c->k_hist.p, sizeof(u32) * r.iters, cudaMemcpyDeviceToHost, c->st));
+  GS_CUDA(cudaMemcpyAsync(c->iter_fp.data(), c->fp_hist.p, sizeof(u64) * r.iters, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  for (int i = 0; i < r.iters; ++i) c->iter_k[i] = kk[i];
+  return r;
+}
+
+RunOut run_engine(gs_ctx* c, const Input& in, int64_t n, int d, double h, double eta, int max_iters,
+                  int64_t* labels_dev, double* movement_out) {
+  switch (d) {
+#define GS_CASE(DD) \
+  case DD:          \
+    return run_engine_d<DD>(c, in, n, h, eta, max_iters, labels_dev, movement_out);
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
+#undef GS_CASE
+  }
+  fail(GS_EUNSUPPORTED, "unsupported d");
+}
+
+void validate_run(int64_t n, int d, double h, double eta, int max_iters) {
+  validate_common(n, d, h);
+  if (!(std::isfinite(eta) && eta > 0)) fail(GS_EINVAL, "eta must be positive and finite");
+  if (max_iters < 1) fail(GS_EINVAL, "max_iters must be a positive integer");
+}
+
+// --------------------------------------------------------------- step / tables
+
+template <int D>
+void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_out_host, double* movement) {
+  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
+  double* y1 = ensure<double>(c, c->y[1], (size_t)n * D);
+  ensure<Ctrl>(c, c->ctrl, 1);
+  Input in{IN_F64, xdev};
+  const InitStats s = run_init<D>(c, in, n, h, y0);
+  Plan p = make_plan(n, D, h, s);
+  Tabs<D> tabs = make_tabs<D>(c, p);
+  ensure<double>(c, c->targets, p.slots * D);
+  const int nb_pts = blocks_for(c, n);
+  const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
+  ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
+  ensure<double>(c, c->mv_hist, 1);
+  ensure<u64>(c, c->fp_hist, 1);
+  ensure<u32>(c, c->k_hist, 1);
+  reset_ctrl(c);
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  if (p.dense) {
+    enqueue_iteration<D>(c, p, tabs.dn, 0, -1.0, n, nb_pts, nb_cells);
+    k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.dn[0], &ctrl->k[0]);
+  } else {
+    enqueue_iteration<D>(c, p, tabs.hs, 0, -1.0, n, nb_pts, nb_cells);
+    k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.hs[0], &ctrl->k[0]);
+  }
+  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]);
+  double* aos = ensure<double>(c, c->x_stage, (size_t)n * D);
+  k_soa_to_aos<D><<<nb_pts, kThreads, 0, c->st>>>(y1, aos, n);
+  check_launch();
+  read_ctrl(c);
+  check_flags(c->h_ctrl->error);
+  GS_CUDA(cudaMemcpyAsync(y_out_host, aos, sizeof(double) * n * D, cudaMemcpyDeviceToHost, c->st));
+  GS_CUDA(cudaMemcpyAsync(movement, c->mv_hist.p, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+}
+
+template <int D, class Tab>
+int64_t dump_tables(gs_ctx* c, const Plan& p, Tab* tabs, int64_t cap, int64_t* cells_out, int64_t* counts_out,
+                    double* sums_out, int64_t* nc_out, double* ns_out) {
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  read_ctrl(c);
+  check_flags(c->h_ctrl->error);
+  const int64_t k = c->h_ctrl->k[0];
+  if (cap >= k && k > 0) {
+    u64* dk = ensure<u64>(c, c->roots, k);
+    i64* dc = ensure<i64>(c, c->root_first, k);
+    double* ds = ensure<double>(c, c->modes, (size_t)k * D);
+    i64* dnc = nullptr;
+    double* dns = nullptr;
+    if (nc_out) {
+      dnc = ensure<i64>(c, c->ranks, k);
+      dns = ensure<double>(c, c->aux, (size_t)k * D);
+    }
+    k_dump<D, Tab><<<blocks_for(c, k), kThreads, 0, c->st>>>(p.g, tabs[0], &ctrl->k[0], dk, dc, ds, dnc, dns);
+    check_launch();
+    std::vector<u64> hk(k);
+    std::vector<i64> hc(k), hnc(nc_out ? k : 0);
+    std::vector<double> hsum((size_t)k * D), hns(nc_out ? (size_t)k * D : 0);
+    GS_CUDA(cudaMemcpyAsync(hk.data(), dk, k * 8, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(hc.data(), dc, k * 8, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(hsum.data(), ds, k * 8 * D, cudaMemcpyDeviceToHost, c->st));
+    if (nc_out) {
+      GS_CUDA(cudaMemcpyAsync(hnc.data(), dnc, k * 8, cudaMemcpyDeviceToHost, c->st));
+      GS_CUDA(cudaMemcpyAsync(hns.data(), dns, k * 8 * D, cudaMemcpyDeviceToHost, c->st));
+    }
+    sync(c);
+    std::vector<int64_t> order(k);
+    for (int64_t i = 0; i < k; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return hk[a] < hk[b]; });
+    for (int64_t r = 0; r < k; ++r) {
+      const int64_t a = order[r];
+      for (int j = 0; j < D; ++j) {
+        const uint64_t ext = (j == 0) ? (p.g.nkeys / p.g.stride[0]) : (p.g.stride[j - 1] / p.g.stride[j]);
+        cells_out[r * D + j] = (int64_t)((hk[a] / p.g.stride[j]) % ext) + p.g.base[j];
+        sums_out[r * D + j] = hsum[a * D + j];
+        if (nc_out) ns_out[r * D + j] = hns[a * D + j];
+      }
+      counts_out[r] = hc[a];
+      if (nc_out) nc_out[r] = hnc[a];
+    }
+  }
+  k_clear<D, Tab><<<blocks_for(c, (int64_t)p.list_cap), kThreads, 0, c->st>>>(tabs[0], &ctrl->k[0]);
+  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]);
+  check_launch();
+  sync(c);
+  return k;
+}
+
+template <int D>
+int64_t run_tables_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t cap, int64_t* cells,
+                     int64_t* counts, double* sums, int64_t* nc, double* ns) {
+  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
+  ensure<Ctrl>(c, c->ctrl, 1);
+  Input in{IN_F64, xdev};
+  const InitStats s = run_init<D>(c, in, n, h, y0);
+  Plan p = make_plan(n, D, h, s);
+  Tabs<D> tabs = make_tabs<D>(c, p);
+  reset_ctrl(c);
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  const int nb_pts = blocks_for(c, n);
+  if (p.dense) {
+    k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.dn[0], ctrl, 0);
+    return dump_tables<D>(c, p, tabs.dn, cap, cells, counts, sums, nc, ns);
+  }
+  k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.hs[0], ctrl, 0);
+  return dump_tables<D>(c, p, tabs.hs, cap, cells, counts, sums, nc, ns);
+}
+
+template <int D>
+int64_t run_extract_only_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t* labels_dev) {
+  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
+  ensure<Ctrl>(c, c->ctrl, 1);
+  Input in{IN_F64, xdev};
+  const InitStats s = run_init<D>(c, in, n, h, y0);
+  Plan p = make_plan(n, D, h, s);
+  Tabs<D> tabs = make_tabs<D>(c, p);
+  reset_ctrl(c);
+  if (p.dense)
+    run_extract<D>(c, p, tabs.dn, y0, n, 0, labels_dev);
+  else
+    run_extract<D>(c, p, tabs.hs, y0, n, 0, labels_dev);
+  return c->k_last;
+}
+
+template <typename F>
+int guarded(gs_ctx* c, F&& f) {
+  g_err.clear();
+  if (!c) {
+    g_err = "null context";
+    return GS_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(c->mu);
+  try {
+    GS_CUDA(cudaSetDevice(c->device));
+    c->st = c->own;
+    f();
+    return GS_OK;
+  } catch (const Fail& e) {
+    // leave the context usable: drain the stream
+    cudaStreamSynchronize(c->st);
+    cudaGetLastError();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GS_ERUNTIME;
+  }
+}
+
+double* stage_input(gs_ctx* c, const double* x, int64_t n, int d) {
+  double* dx = ensure<double>(c, c->x_stage, (size_t)n * d);
+  GS_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * n * d, cudaMemcpyHostToDevice, c->st));
+  return dx;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+
+extern "C" {
+
+const char* gs_last_error(void) { return g_err.c_str(); }
+
+const char* gs_version(void) { return "gridshift-b200 0.1 sm_100a"; }
+
+int gs_ctx_create(int device, gs_ctx** out) {
+  g_err.clear();
+  if (!out) return GS_EINVAL;
+  *out = nullptr;
+  gs_ctx* c = new gs_ctx();
+  try {
+    c->device = device;
+    GS_CUDA(cudaSetDevice(device));
+    GS_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+    GS_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->st = c->own;
+    GS_CUDA(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)));
+    GS_CUDA(cudaMallocHost(&c->h_stats, sizeof(InitStats)));
+    GS_CUDA(cudaMallocHost(&c->h_small, 64));
+    ensure<Ctrl>(c, c->ctrl, 1);
+    sync(c);
+  } catch (const Fail& e) {
+    delete c;
+    return e.code;
+  }
+  *out = c;
+  return GS_OK;
+}
+
+void gs_ctx_destroy(gs_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->own) cudaStreamSynchronize(c->own);
+  Buf* bufs[] = {&c->x_stage, &c->y[0], &c->y[1], &c->ent[0], &c->ent[1], &c->keys[0], &c->keys[1],
+                 &c->list[0], &c->list[1], &c->targets, &c->partials, &c->par, &c->first, &c->aux,
+                 &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
+                 &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
+                 &c->track_out, &c->bitmaps};
+  for (Buf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+  if (c->h_stats) cudaFreeHost(c->h_stats);
+  if (c->h_small) cudaFreeHost(c->h_small);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+int gs_meanshiftpp(gs_ctx* c, const double* x, int64_t n, int32_t d, double h, double eta,
+                   int32_t max_iters, int64_t* labels_out, int64_t* k_out, int32_t* iters_out,
+                   double* movement_out, int32_t* converged_out) {
+  return guarded(c, [&] {
+    validate_run(n, d, h, eta, max_iters);
+    if (!x || !labels_out) fail(GS_EINVAL, "null buffer");
+    const double* dx = stage_input(c, x, n, d);
+    int64_t* dl = ensure<int64_t>(c, c->labels, n);
+    Input in{IN_F64, dx};
+    RunOut r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
+    GS_CUDA(cudaMemcpyAsync(labels_out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (k_out) *k_out = r.k;
+    if (iters_out) *iters_out = r.iters;
+    if (converged_out) *converged_out = r.converged;
+  });
+}
+
+int gs_meanshiftpp_device(gs_ctx* c, const void* x_dev, int32_t dtype, int64_t n, int32_t d, double h,
+                          double eta, int32_t max_iters, int64_t* labels_dev, int64_t* k_out,
+                          int32_t* iters_out, double* movement_out, int32_t* converged_out, void* stream) {
+  return guarded(c, [&] {
+    validate_run(n, d, h, eta, max_iters);
+    if (!x_dev || !labels_dev) fail(GS_EINVAL, "null buffer");
+    if (dtype != GS_DTYPE_F64 && dtype != GS_DTYPE_F32) fail(GS_EINVAL, "dtype must be f64 or f32");
+    if (stream) c->st = static_cast<cudaStream_t>(stream);
+    Input in{dtype == GS_DTYPE_F64 ? IN_F64 : IN_F32, x_dev};
+    RunOut r = run_engine(c, in, n, d, h, eta, max_iters, labels_dev, movement_out);
+    sync(c);
+    if (k_out) *k_out = r.k;
+    if (iters_out) *iters_out = r.iters;
+    if (converged_out) *converged_out = r.converged;
+  });
+}
+
+int gs_segment_image(gs_ctx* c, const uint8_t* pixels, int32_t height, int32_t width, int32_t mode,
+                     double scale, double h, double eta, int32_t max_iters, int64_t* labels_out,
+                     int64_t* k_out, int32_t* iters_out, double* movement_out, int32_t* converged_out) {
+  return guarded(c, [&] {
+    if (height < 1 || width < 1) fail(GS_EINVAL, "image must contain at least one pixel");
+    if (mode != 0 && mode != 1) fail(GS_EINVAL, "mode must be one of ('rgb', 'rgbxy')");
+    const int64_t n = (int64_t)height * width;
+    const int d = mode == 0 ? 3 : 5;
+    validate_run(n, d, h, eta, max_iters);
+    if (!std::isfinite(scale)) fail(GS_EINVAL, "point data contains NaN or infinite entries");
+    unsigned char* dp = ensure<unsigned char>(c, c->x_stage, (size_t)n * 3);
+    GS_CUDA(cudaMemcpyAsync(dp, pixels, (size_t)n * 3, cudaMemcpyHostToDevice, c->st));
+    int64_t* dl = ensure<int64_t>(c, c->labels, n);
+    Input in{IN_IMAGE, dp, width, scale};
+    RunOut r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
+    GS_CUDA(cudaMemcpyAsync(labels_out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (k_out) *k_out = r.k;
+    if (iters_out) *iters_out = r.iters;
+    if (converged_out) *converged_out = r.converged;
+  });
+}
+
+int gs_fetch_modes(gs_ctx* c, double* modes_out, int64_t cap_rows) {
+  return guarded(c, [&] {
+    if (cap_rows < c->k_last) fail(GS_EINVAL, "modes buffer too small");
+    memcpy(modes_out, c->modes_host.data(), sizeof(double) * c->modes_host.size());
+  });
+}
+
+int gs_fetch_trace(gs_ctx* c, int64_t* k_per_iter, uint64_t* fp_per_iter, int32_t cap) {
+  return guarded(c, [&] {
+    const int m = std::min<int>(cap, (int)c->iter_k.size());
+    for (int i = 0; i < m; ++i) {
+      if (k_per_iter) k_per_iter[i] = c->iter_k[i];
+      if (fp_per_iter) fp_per_iter[i] = c->iter_fp[i];
+    }
+  });
+}
+
+int gs_shift_step(gs_ctx* c, const double* y, int64_t n, int32_t d, double h, double* y_out,
+                  double* movement_out) {
+  return guarded(c, [&] {
+    validate_common(n, d, h);
+    const double* dx = stage_input(c, y, n, d);
+    switch (d) {
+#define GS_CASE(DD) \
+  case DD:          \
+    run_step_d<DD>(c, dx, n, h, y_out, movement_out); \
+    break;
+      GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
+#undef GS_CASE
+    }
+  });
+}
+
+int gs_build_tables(gs_ctx* c, const double* y, int64_t n, int32_t d, double h, int64_t cap,
+                    int64_t* cells_out, int64_t* counts_out, double* sums_out, int64_t* nbr_counts_out,
+                    double* nbr_sums_out, int64_t* k_out) {
+  return guarded(c, [&] {
+    validate_common(n, d, h);
+    const double* dx = stage_input(c, y, n, d);
+    int64_t k = 0;
+    switch (d) {
+#define GS_CASE(DD) \
+  case DD:          \
+    k = run_tables_d<DD>(c, dx, n, h, cap, cells_out, counts_out, sums_out, nbr_counts_out, nbr_sums_out); \
+    break;
+      GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
+#undef GS_CASE
+    }
+    if (k_out) *k_out = k;
+  });
+}
+
+int gs_extract_clusters(gs_ctx* c, const double* y, int64_t n, int32_t d, double h, int64_t* labels_out,
+                        int64_t* k_out) {
+  return guarded(c, [&] {
+    validate_common(n, d, h);
+    const double* dx = stage_input(c, y, n, d);
+    int64_t* dl = ensure<int64_t>(c, c->labels, n);
+    int64_t k = 0;
+    switch (d) {
+#define GS_CASE(DD) \
+  case DD:          \
+    k = run_extract_only_d<DD>(c, dx, n, h, dl); \
+    break;
+      GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
+#undef GS_CASE
+    }
+    GS_CUDA(cudaMemcpyAsync(labels_out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (k_out) *k_out = k;
+  });
+}
+
+int gs_track_sequence(gs_ctx* c, const uint8_t* frames, int32_t n_frames, int32_t height, int32_t width,
+                      double cx, double cy, int32_t w, int32_t h_px, const int64_t* bins, int32_t nb,
+                      double h, int32_t update_bins, int32_t init_matches, double tol, int32_t max_iters,
+                      double* cx_out, double* cy_out, int32_t* lost_out, int64_t* matches_out,
+                      int64_t* nbins_out, uint32_t* bitmap_hist_out) {
+  return guarded(c, [&] {
+    if (!(std::isfinite(h) && h > 0.0)) fail(GS_EINVAL, "bandwidth must be a positive finite real");
+    if (n_frames < 1 || height < 1 || width < 1) fail(GS_EINVAL, "need at least one non-empty frame");
+    if (w < 1 || h_px < 1) fail(GS_EINVAL, "window extents must be positive");
+    if (nb < 1) fail(GS_EINVAL, "bin set cannot be empty");
+    if (max_iters < 1) fail(GS_EINVAL, "max_iters must be positive");
+    const double Ld = std::floor(255.0 / h) + 1.0;
+    if (Ld > 645.0) fail(GS_EUNSUPPORTED, "colour bandwidth too small for the bitmap bin set");
+    const int L = (int)Ld;
+    const int64_t cells = (int64_t)L * L * L;
+    const int words = (int)((cells + 31) / 32);
+    std::vector<u32> bm(words, 0u);
+    for (int i = 0; i < nb; ++i) {
+      const int64_t a = bins[3 * i], b = bins[3 * i + 1], cc = bins[3 * i + 2];
+      if (a < 0 || b < 0 || cc < 0 || a >= L || b >= L || cc >= L)
+        fail(GS_EINVAL, "bin set holds a colour cell outside [0, floor(255/h)]^3");
+      const int64_t code = (a * L + b) * L + cc;
+      bm[code >> 5] |= 1u << (code & 31);
+    }
+    int lut[256];
+    for (int v = 0; v < 256; ++v) lut[v] = (int)std::floor((double)v / h);
+    const size_t fbytes = (size_t)n_frames * height * width * 3;
+    unsigned char* df = ensure<unsigned char>(c, c->track, fbytes);
+    GS_CUDA(cudaMemcpyAsync(df, frames, fbytes, cudaMemcpyHostToDevice, c->st));
+    u32* dbm = ensure<u32>(c, c->bitmaps, (2 + (size_t)n_frames) * words + 256);
+    int* dlut = reinterpret_cast<int*>(dbm + 2 * words);
+    u32* dhist = dbm + 2 * words + 256;
+    GS_CUDA(cudaMemcpyAsync(dhist, bm.data(), words * sizeof(u32), cudaMemcpyHostToDevice, c->st));
+    GS_CUDA(cudaMemcpyAsync(dbm, bm.data(), words * sizeof(u32), cudaMemcpyHostToDevice, c->st));
+    GS_CUDA(cudaMemcpyAsync(dlut, lut, sizeof lut, cudaMemcpyHostToDevice, c->st));
+    const size_t T = (size_t)n_frames;
+    char* o = ensure<char>(c, c->track_out, T * (8 + 8 + 4 + 8 + 8) + 64);
+    double* dcx = reinterpret_cast<double*>(o);
+    double* dcy = dcx + T;
+    long long* dm = reinterpret_cast<long long*>(dcy + T);
+    long long* dnb = dm + T;
+    int* dlost = reinterpret_cast<int*>(dnb + T);
+    // row 0 = the init state (track.py:199-200)
+    const double r0[2] = {cx, cy};
+    const long long m0[2] = {init_matches, nb};
+    const int l0 = 0;
+    GS_CUDA(cudaMemcpyAsync(dcx, &r0[0], 8, cudaMemcpyHostToDevice, c->st));
+    GS_CUDA(cudaMemcpyAsync(dcy, &r0[1], 8, cudaMemcpyHostToDevice, c->st));
+    GS_CUDA(cudaMemcpyAsync(dm, &m0[0], 8, cudaMemcpyHostToDevice, c->st));
+    GS_CUDA(cudaMemcpyAsync(dnb, &m0[1], 8, cudaMemcpyHostToDevice, c->st));
+    GS_CUDA(cudaMemcpyAsync(dlost, &l0, 4, cudaMemcpyHostToDevice, c->st));
+    TrackParams tp{};
+    tp.n_frames = n_frames;
+    tp.height = height;
+    tp.width = width;
+    tp.w = w;
+    tp.hp = h_px;
+    tp.L = L;
+    tp.update_bins = update_bins ? 1 : 0;
+    tp.max_iters = max_iters;
+    tp.tol = tol;
+    tp.cx0 = cx;
+    tp.cy0 = cy;
+    tp.words = words;
+    tp.init_matches = init_matches;
+    k_track<<<1, kTrackThreads, 0, c->st>>>(df, tp, dlut, dbm, dbm + words, dcx, dcy, dlost, dm, dnb,
+                                            dhist);
+    check_launch();
+    GS_CUDA(cudaMemcpyAsync(cx_out, dcx, 8 * T, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(cy_out, dcy, 8 * T, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(matches_out, dm, 8 * T, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(nbins_out, dnb, 8 * T, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(lost_out, dlost, 4 * T, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(bm.data(), dbm, words * sizeof(u32), cudaMemcpyDeviceToHost, c->st));
+    if (bitmap_hist_out)
+      GS_CUDA(cudaMemcpyAsync(bitmap_hist_out, dhist, T * words * sizeof(u32), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    c->track_bins.clear();
+    for (int64_t code = 0; code < cells; ++code)
+      if ((bm[code >> 5] >> (code & 31)) & 1u) {
+        c->track_bins.push_back(code / ((int64_t)L * L));
+        c->track_bins.push_back((code / L) % L);
+        c->track_bins.push_back(code % L);
+      }
+  });
+}
+
+int gs_fetch_track_bins(gs_ctx* c, int64_t* bins_out, int32_t cap, int32_t* nb_out) {
+  return guarded(c, [&] {
+    const int32_t nb = (int32_t)(c->track_bins.size() / 3);
+    if (nb_out) *nb_out = nb;
+    if (bins_out && cap >= nb) memcpy(bins_out, c->track_bins.data(), c->track_bins.size() * 8);
+  });
+}
+
+}  // extern "C"

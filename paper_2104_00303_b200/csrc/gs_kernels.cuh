@@ -1,0 +1,689 @@
+// gridshift-b200: sm_100a kernels for the MeanShift++ grid shift.
+//
+// Per iteration t (table buffer b = t & 1, reference modeseek.py:105-111):
+//   k_hist   : bin every point (floor(y/h), grid.py:78-85), pack its cell key
+//              (grid.py:137-158), and accumulate count + exact fixed-point
+//              coordinate sums into the cell table (grid.py:179-190).
+//              Warp-aggregated: lanes holding the same key form segments and
+//              only the segment head touches the table.
+//   k_agg    : per occupied cell, the 3^d neighbourhood count and exact sum
+//              (grid.py:230-259), rounded once and divided -> the cell's
+//              target mean (modeseek.py:109).  Also clears table b^1 and
+//              folds the per-iteration (cells, counts) fingerprint.
+//   k_shift  : per point, look up its cell's target, write y', and sum the
+//              per-point L2 movement in 128-bit fixed point
+//              (modeseek.py:110); the last CTA finishes the reduction and
+//              evaluates `movement < eta` (modeseek.py:139) on device.
+// Extraction (modeseek.py:229-272): hist of the final iterate, lock-free
+// union-find over Chebyshev-adjacent occupied cells, first-appearance
+// minimum per component, dense relabel, exact per-component means.
+#pragma once
+
+#include "gs_common.cuh"
+
+namespace gs {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------ tables
+
+template <int D>
+struct DenseTable {
+  static constexpr bool kDense = true;
+  Entry<D>* ent;
+  u32* list;      // occupied slots, in first-touch order
+  u32* k;         // occupied count (device)
+  __device__ __forceinline__ u64 key_of(u32 s) const { return s; }
+  __device__ __forceinline__ bool find(u64 key, u32& s) const {
+    s = (u32)key;
+    return ent[key].count != 0;
+  }
+  __device__ __forceinline__ u32 lookup(u64 key) const { return (u32)key; }
+  __device__ __forceinline__ u32 insert(u64 key, bool& fresh, int*) const {
+    fresh = false;
+    return (u32)key;
+  }
+};
+
+template <int D>
+struct HashTable {
+  static constexpr bool kDense = false;
+  Entry<D>* ent;
+  u32* list;
+  u32* k;
+  u64* keys;      // kEmpty when free
+  u64 mask;
+  __device__ __forceinline__ u64 key_of(u32 s) const { return keys[s]; }
+  __device__ __forceinline__ bool find(u64 key, u32& s) const {
+    u64 p = hash_key(key) & mask;
+    for (u64 probe = 0; probe <= mask; ++probe) {
+      const u64 kk = keys[p];
+      if (kk == key) { s = (u32)p; return true; }
+      if (kk == kEmpty) return false;
+      p = (p + 1) & mask;
+    }
+    return false;
+  }
+  __device__ __forceinline__ u32 lookup(u64 key) const {
+    u32 s = 0;
+    find(key, s);
+    return s;
+  }
+  __device__ __forceinline__ u32 insert(u64 key, bool& fresh, int* err) const {
+    u64 p = hash_key(key) & mask;
+    for (u64 probe = 0; probe <= mask; ++probe) {
+      u64 kk = *(volatile u64*)(keys + p);
+      if (kk == kEmpty) {
+        kk = atomicCAS(keys + p, kEmpty, key);
+        if (kk == kEmpty) { fresh = true; return (u32)p; }
+      }
+      if (kk == key) { fresh = false; return (u32)p; }
+      p = (p + 1) & mask;
+    }
+    atomicOr(err, kErrTableFull);
+    fresh = false;
+    return 0xffffffffu;
+  }
+};
+
+// --------------------------------------------------------------- helpers
+
+// Row sum in numpy's add.reduce order (pairwise_sum: sequential below 8
+// elements, an 8-way tree at exactly 8) -- modeseek.py:110 `.sum(axis=1)`.
+template <int D>
+__device__ __forceinline__ double row_sum(const double* a) {
+  if constexpr (D < 8) {
+    double r = a[0];
+#pragma unroll
+    for (int j = 1; j < D; ++j) r = __dadd_rn(r, a[j]);
+    return r;
+  } else {
+    return __dadd_rn(__dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3])),
+                     __dadd_rn(__dadd_rn(a[4], a[5]), __dadd_rn(a[6], a[7])));
+  }
+}
+
+template <int D>
+__device__ __forceinline__ u64 cell_fingerprint(const GridParams& g, u64 key, u64 count) {
+  u64 x = 0x9E3779B97F4A7C15ull * (u64)(D + 1);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const u64 ext = (j == 0) ? (g.nkeys / g.stride[0]) : (g.stride[j - 1] / g.stride[j]);
+    const i64 c = (i64)((key / g.stride[j]) % ext) + g.base[j];
+    x = mix64(x ^ (u64)c);
+  }
+  return mix64(x ^ count);
+}
+
+// Pack the cell of one point.  Returns kEmpty if the cell is outside the
+// admissible box (flags the error; never happens for valid runs).
+template <int D>
+__device__ __forceinline__ u64 pack_key(const GridParams& g, const double* v, bool& inside) {
+  u64 key = 0;
+  inside = true;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const i64 c = (i64)cell_of(v[j], g.h);
+    inside &= (c >= g.lo[j]) & (c <= g.hi[j]);
+    key += (u64)(c - g.base[j]) * g.stride[j];
+  }
+  return inside ? key : kEmpty;
+}
+
+__device__ __forceinline__ void add128(u64& hi, u64& lo, u64 ohi, u64 olo) {
+  const u64 l = lo + olo;
+  hi += ohi + (l < lo ? 1ull : 0ull);
+  lo = l;
+}
+
+// --------------------------------------------------------------- k_init
+// AoS (n, d) input (fp64 or fp32) -> SoA fp64 iterate, plus the per-axis
+// cell range, max |coordinate| and input validity (grid.py:42-51, 78-85).
+
+struct InitStats {
+  i64 cmin[GS_MAXD];
+  i64 cmax[GS_MAXD];
+  u64 absmax[GS_MAXD];   // bit pattern of max |x| (non-negative doubles order as ints)
+  int flags;
+  int pad;
+};
+
+template <int D, typename T>
+__global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, double* __restrict__ y,
+                                                       i64 n, double h, InitStats* st) {
+  i64 cmin[D], cmax[D];
+  u64 amax[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) { cmin[j] = LLONG_MAX; cmax[j] = LLONG_MIN; amax[j] = 0; }
+  int flags = 0;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double v = (double)x[i * D + j];
+      y[(i64)j * n + i] = v;
+      if (!isfinite(v)) { flags |= kErrNonFinite; continue; }
+      const double c = cell_of(v, h);
+      if (fabs(c) >= 4611686018427387904.0) { flags |= kErrLattice; continue; }
+      const i64 ci = (i64)c;
+      cmin[j] = min(cmin[j], ci);
+      cmax[j] = max(cmax[j], ci);
+      amax[j] = max(amax[j], (u64)__double_as_longlong(fabs(v)));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    for (int o = 16; o; o >>= 1) {
+      cmin[j] = min(cmin[j], (i64)__shfl_xor_sync(kFull, (unsigned long long)cmin[j], o));
+      cmax[j] = max(cmax[j], (i64)__shfl_xor_sync(kFull, (unsigned long long)cmax[j], o));
+      amax[j] = max(amax[j], (u64)__shfl_xor_sync(kFull, amax[j], o));
+    }
+  }
+  for (int o = 16; o; o >>= 1) flags |= __shfl_xor_sync(kFull, flags, o);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      atomicMin((long long*)&st->cmin[j], (long long)cmin[j]);
+      atomicMax((long long*)&st->cmax[j], (long long)cmax[j]);
+      atomicMax((unsigned long long*)&st->absmax[j], (unsigned long long)amax[j]);
+    }
+    if (flags) atomicOr(&st->flags, flags);
+  }
+}
+
+// uint8 image (H, W, 3) -> rgb or rgbxy features (segment.py:82-92), fused.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_init_image(const unsigned char* __restrict__ px, double* __restrict__ y,
+                                                         i64 n, int width, double scale, double h, InitStats* st) {
+  i64 cmin[D], cmax[D];
+  u64 amax[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) { cmin[j] = LLONG_MAX; cmax[j] = LLONG_MIN; amax[j] = 0; }
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v[D];
+    v[0] = (double)px[i * 3 + 0];
+    v[1] = (double)px[i * 3 + 1];
+    v[2] = (double)px[i * 3 + 2];
+    if constexpr (D == 5) {
+      const i64 row = i / width;
+      const i64 col = i - row * width;
+      v[3] = __dmul_rn((double)col, scale);
+      v[4] = __dmul_rn((double)row, scale);
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      y[(i64)j * n + i] = v[j];
+      const i64 ci = (i64)cell_of(v[j], h);
+      cmin[j] = min(cmin[j], ci);
+      cmax[j] = max(cmax[j], ci);
+      amax[j] = max(amax[j], (u64)__double_as_longlong(fabs(v[j])));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    for (int o = 16; o; o >>= 1) {
+      cmin[j] = min(cmin[j], (i64)__shfl_xor_sync(kFull, (unsigned long long)cmin[j], o));
+      cmax[j] = max(cmax[j], (i64)__shfl_xor_sync(kFull, (unsigned long long)cmax[j], o));
+      amax[j] = max(amax[j], (u64)__shfl_xor_sync(kFull, amax[j], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      atomicMin((long long*)&st->cmin[j], (long long)cmin[j]);
+      atomicMax((long long*)&st->cmax[j], (long long)cmax[j]);
+      atomicMax((unsigned long long*)&st->absmax[j], (unsigned long long)amax[j]);
+    }
+  }
+}
+
+// SoA fp64 -> AoS fp64 (meanshiftpp_step output).
+template <int D>
+__global__ void k_soa_to_aos(const double* __restrict__ y, double* __restrict__ x, i64 n) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[i * D + j] = y[(i64)j * n + i];
+  }
+}
+
+// --------------------------------------------------------------- k_hist
+
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y, i64 n, GridParams g,
+                                                   Tab tab, Ctrl* ctrl, int check_done) {
+  if (check_done && *(volatile int*)&ctrl->done) return;
+  const int lane = threadIdx.x & 31;
+  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 base = warp * 32; base < n; base += nwarps * 32) {
+    const i64 i = base + lane;
+    u64 key = kEmpty;
+    i64 fx[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) fx[j] = 0;
+    if (i < n) {
+      double v[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * n + i);
+      bool inside;
+      key = pack_key<D>(g, v, inside);
+      if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+#pragma unroll
+      for (int j = 0; j < D; ++j) fx[j] = to_fixed(v[j], g.qscale[j]);
+    }
+    // segments: maximal runs of consecutive lanes with the same key
+    const u64 pkey = __shfl_up_sync(kFull, key, 1);
+    const bool same_prev = (lane > 0) && (pkey == key);
+    bool same_val = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) same_val &= ((i64)__shfl_up_sync(kFull, (unsigned long long)fx[j], 1) == fx[j]);
+    const u32 heads = __ballot_sync(kFull, !same_prev);
+    const u32 mixed = __ballot_sync(kFull, same_prev && !same_val);
+    const u32 after = (lane == 31) ? 0u : (heads & (~0u << (lane + 1)));
+    const int end = after ? (__ffs(after) - 1) : 32;
+    i64 shi[D];
+    u64 slo[D];
+    if (mixed == 0) {
+      // every segment carries one value: head contributes count * value
+      const i64 cnt = end - lane;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        shi[j] = (fx[j] >> 32) * cnt;
+        slo[j] = (u64)(fx[j] & 0xffffffffll) * (u64)cnt;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        shi[j] = fx[j] >> 32;
+        slo[j] = (u64)(fx[j] & 0xffffffffll);
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const i64 oh = (i64)__shfl_down_sync(kFull, (unsigned long long)shi[j], off);
+          const u64 ol = __shfl_down_sync(kFull, slo[j], off);
+          if (lane + off < end) { shi[j] += oh; slo[j] += ol; }
+        }
+      }
+    }
+    if (!same_prev && key != kEmpty) {
+      const u64 cnt = (u64)(end - lane);
+      bool fresh;
+      const u32 s = tab.insert(key, fresh, &ctrl->error);
+      if (s != 0xffffffffu) {
+        Entry<D>* e = tab.ent + s;
+        const u64 old = atomicAdd(&e->count, cnt);
+        if (Tab::kDense ? (old == 0) : fresh) tab.list[atomicAdd(tab.k, 1u)] = s;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          atomicAdd(&e->hi[j], (u64)shi[j]);
+          atomicAdd(&e->lo[j], slo[j]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- k_agg
+
+template <int D, class Tab>
+__device__ __forceinline__ void neighbourhood_sum(const GridParams& g, const Tab& tab, u64 key,
+                                                  u64& cnt, i128* sum) {
+  constexpr int M = (D == 1) ? 3 : (D == 2) ? 9 : (D == 3) ? 27 : (D == 4) ? 81 :
+                    (D == 5) ? 243 : (D == 6) ? 729 : (D == 7) ? 2187 : 6561;
+  cnt = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) sum[j] = 0;
+  for (int o = 0; o < M; ++o) {
+    int r = o;
+    i64 delta = 0;
+#pragma unroll
+    for (int j = D - 1; j >= 0; --j) {
+      delta += (i64)((r % 3) - 1) * (i64)g.stride[j];
+      r /= 3;
+    }
+    u32 ns;
+    if (tab.find(key + (u64)delta, ns)) {
+      const Entry<D>& e = tab.ent[ns];
+      cnt += e.count;
+#pragma unroll
+      for (int j = 0; j < D; ++j) sum[j] += (((i128)(i64)e.hi[j]) << 32) + (i128)e.lo[j];
+    }
+  }
+}
+
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab prev, double* __restrict__ targets,
+                                                  Ctrl* ctrl, int cur, u64* fp_out, u32* k_out) {
+  if (*(volatile int*)&ctrl->done) return;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  // clear the previous iteration's table (no longer referenced)
+  const u32 kp = ctrl->k[cur ^ 1];
+  for (i64 a = tid; a < kp; a += stride) {
+    const u32 s = prev.list[a];
+    Entry<D>* e = prev.ent + s;
+    e->count = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { e->hi[j] = 0; e->lo[j] = 0; }
+    if constexpr (!Tab::kDense) prev.keys[s] = kEmpty;
+  }
+  const u32 k = ctrl->k[cur];
+  u64 fp = 0;
+  for (i64 a = tid; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    const u64 key = tab.key_of(s);
+    u64 cnt;
+    i128 sum[D];
+    neighbourhood_sum<D>(g, tab, key, cnt, sum);
+    const double c = (double)cnt;
+#pragma unroll
+    for (int j = 0; j < D; ++j) targets[(i64)s * D + j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
+    fp += cell_fingerprint<D>(g, key, tab.ent[s].count);
+  }
+  for (int o = 16; o; o >>= 1) fp += __shfl_xor_sync(kFull, fp, o);
+  if ((threadIdx.x & 31) == 0 && fp) atomicAdd((unsigned long long*)fp_out, (unsigned long long)fp);
+  if (tid == 0 && k_out) *k_out = k;
+}
+
+// -------------------------------------------------------------- k_shift
+
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
+                                                    GridParams g, Tab tab, const double* __restrict__ targets,
+                                                    Ctrl* ctrl, u64* partials, double* mv_hist, int t,
+                                                    double eta, int cur) {
+  if (*(volatile int*)&ctrl->done) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->k[cur ^ 1] = 0;
+  u64 ahi = 0, alo = 0;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * n + i);
+    bool inside;
+    const u64 key = pack_key<D>(g, v, inside);
+    u32 s;
+    if (!inside || !tab.find(key, s)) {
+      atomicOr(&ctrl->error, kErrMissing);
+      continue;
+    }
+    double sq[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double nv = targets[(i64)s * D + j];
+      __stcs(yo + (i64)j * n + i, nv);
+      const double dlt = __dsub_rn(nv, v[j]);
+      sq[j] = __dmul_rn(dlt, dlt);
+    }
+    const u128 f = norm_to_fixed(__dsqrt_rn(row_sum<D>(sq)), g.movement_exp);
+    add128(ahi, alo, (u64)(f >> 64), (u64)f);
+  }
+  // block reduction of the 128-bit movement
+  for (int o = 16; o; o >>= 1) {
+    const u64 oh = __shfl_xor_sync(kFull, ahi, o);
+    const u64 ol = __shfl_xor_sync(kFull, alo, o);
+    add128(ahi, alo, oh, ol);
+  }
+  __shared__ u64 sh[kThreads / 32][2];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sh[w][0] = ahi; sh[w][1] = alo; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 bh = 0, bl = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    partials[2 * blockIdx.x] = bh;
+    partials[2 * blockIdx.x + 1] = bl;
+    __threadfence();
+    const u32 ticket = atomicAdd(&ctrl->blocks_done, 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  // last CTA: fixed-order reduction over the partials
+  u64 th = 0, tl = 0;
+  for (u32 b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+    add128(th, tl, __ldcg(partials + 2 * b), __ldcg(partials + 2 * b + 1));
+  for (int o = 16; o; o >>= 1) {
+    const u64 oh = __shfl_xor_sync(kFull, th, o);
+    const u64 ol = __shfl_xor_sync(kFull, tl, o);
+    add128(th, tl, oh, ol);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) { sh[w][0] = th; sh[w][1] = tl; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 bh = 0, bl = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
+    mv_hist[t] = mv;
+    ctrl->iters = t + 1;
+    ctrl->blocks_done = 0;
+    if (mv < eta) ctrl->done = 1;
+  }
+}
+
+// ------------------------------------------------------------- extraction
+
+__device__ __forceinline__ u32 uf_root(u32* par, u32 v) {
+  u32 curr = *(volatile u32*)(par + v);
+  if (curr != v) {
+    u32 prev = v, next;
+    while (curr > (next = *(volatile u32*)(par + curr))) {
+      par[prev] = next;   // path halving; benign race (parents only decrease)
+      prev = curr;
+      curr = next;
+    }
+  }
+  return curr;
+}
+
+__device__ __forceinline__ void uf_unite(u32* par, u32 a, u32 b) {
+  u32 ra = uf_root(par, a), rb = uf_root(par, b);
+  while (ra != rb) {
+    if (ra < rb) { const u32 t = ra; ra = rb; rb = t; }
+    const u32 old = atomicCAS(par + ra, ra, rb);   // hook the larger root
+    if (old == ra) return;
+    ra = uf_root(par, old);
+    rb = uf_root(par, rb);
+  }
+}
+
+template <int D, class Tab>
+__global__ void k_uf_init(Tab tab, const u32* kp, u32* par, u32* first) {
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    par[s] = s;
+    first[s] = 0xffffffffu;
+  }
+}
+
+template <int D, class Tab>
+__global__ void k_uf_link(GridParams g, Tab tab, const u32* kp, u32* par) {
+  constexpr int M = (D == 1) ? 3 : (D == 2) ? 9 : (D == 3) ? 27 : (D == 4) ? 81 :
+                    (D == 5) ? 243 : (D == 6) ? 729 : (D == 7) ? 2187 : 6561;
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    const u64 key = tab.key_of(s);
+    // offsets are symmetric: linking only to lexicographically later
+    // neighbours (o > M/2) covers every adjacent pair once
+    for (int o = M / 2 + 1; o < M; ++o) {
+      int r = o;
+      i64 delta = 0;
+#pragma unroll
+      for (int j = D - 1; j >= 0; --j) {
+        delta += (i64)((r % 3) - 1) * (i64)g.stride[j];
+        r /= 3;
+      }
+      u32 ns;
+      if (tab.find(key + (u64)delta, ns)) uf_unite(par, s, ns);
+    }
+  }
+}
+
+// Component root per occupied cell + exact per-component count/sums
+// (accumulated into the clean scratch entries `acc`, indexed by root slot).
+template <int D, class Tab>
+__global__ void k_uf_flatten(Tab tab, const u32* kp, u32* par, Entry<D>* acc) {
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    const u32 r = uf_root(par, s);
+    par[s] = r;   // unions are complete: flattening is race-free
+    const Entry<D>& e = tab.ent[s];
+    Entry<D>* c = acc + r;
+    atomicAdd(&c->count, e.count);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      atomicAdd(&c->hi[j], e.hi[j]);
+      atomicAdd(&c->lo[j], e.lo[j]);
+    }
+  }
+}
+
+// First appearance: minimum original point index per component
+// (modeseek.py:262-265).  par[] is flat here (k_uf_flatten), so the
+// component of a cell is one load; lanes sharing a component are reduced
+// with match_any + reduce_min before the single atomicMin.
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_first(const double* __restrict__ y, i64 n, GridParams g, Tab tab,
+                                                    const u32* par, u32* first, const u32* perm, Ctrl* ctrl) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 base = warp * 32; base < n; base += nwarps * 32) {
+    const i64 i = base + lane;
+    u32 r = 0xffffffffu, idx = 0xffffffffu;
+    if (i < n) {
+      double v[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = y[(i64)j * n + i];
+      bool inside;
+      const u64 key = pack_key<D>(g, v, inside);
+      u32 s;
+      if (inside && tab.find(key, s)) {
+        r = par[s];
+        idx = perm ? perm[i] : (u32)i;
+      } else {
+        atomicOr(&ctrl->error, kErrMissing);
+      }
+    }
+    const unsigned peers = __match_any_sync(kFull, r);
+    const u32 best = __reduce_min_sync(peers, idx);
+    if (r != 0xffffffffu && lane == __ffs(peers) - 1) atomicMin(first + r, best);
+  }
+}
+
+template <int D, class Tab>
+__global__ void k_roots(Tab tab, const u32* kp, const u32* par, const u32* first, u32* roots,
+                        u32* root_first, u32* nroots) {
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    if (par[s] == s) {
+      const u32 idx = atomicAdd(nroots, 1u);
+      roots[idx] = s;
+      root_first[idx] = first[s];
+    }
+  }
+}
+
+// rank[] for roots (host-sorted by first appearance) -> rankmap[slot];
+// modes = exact component sum / count (modeseek.py:268-271).
+template <int D>
+__global__ void k_modes(GridParams g, const u32* roots, const u32* ranks, u32 nr, u32* rankmap,
+                        Entry<D>* acc, double* modes) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < nr; a += stride) {
+    const u32 r = roots[a];
+    const u32 rk = ranks[a];
+    rankmap[r] = rk;
+    Entry<D>* c = acc + r;
+    const double cnt = (double)c->count;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const i128 s = (((i128)(i64)c->hi[j]) << 32) + (i128)c->lo[j];
+      modes[(i64)rk * D + j] = __ddiv_rn(i128_to_double(s, -g.qexp[j]), cnt);
+      c->hi[j] = 0;
+      c->lo[j] = 0;
+    }
+    c->count = 0;
+  }
+}
+
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_labels(const double* __restrict__ y, i64 n, GridParams g, Tab tab,
+                                                     const u32* par, const u32* rankmap, const u32* perm,
+                                                     i64* labels) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = y[(i64)j * n + i];
+    bool inside;
+    const u64 key = pack_key<D>(g, v, inside);
+    u32 s = 0;
+    if (inside) tab.find(key, s);
+    const u32 r = par[s];
+    const i64 idx = perm ? (i64)perm[i] : i;
+    labels[idx] = (i64)rankmap[r];
+  }
+}
+
+// Clear a table's occupied entries (and keys) and reset its count.
+template <int D, class Tab>
+__global__ void k_clear(Tab tab, u32* kp) {
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    Entry<D>* e = tab.ent + s;
+    e->count = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { e->hi[j] = 0; e->lo[j] = 0; }
+    if constexpr (!Tab::kDense) tab.keys[s] = kEmpty;
+  }
+}
+
+__global__ void k_reset_count(u32* kp) { *kp = 0; }
+
+// Occupied-cell dump for build_cell_tables / neighbour stats (grid.py:193, 230).
+template <int D, class Tab>
+__global__ void k_dump(GridParams g, Tab tab, const u32* kp, u64* keys_out, i64* counts_out,
+                       double* sums_out, i64* ncounts_out, double* nsums_out) {
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    const u64 key = tab.key_of(s);
+    keys_out[a] = key;
+    const Entry<D>& e = tab.ent[s];
+    counts_out[a] = (i64)e.count;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const i128 v = (((i128)(i64)e.hi[j]) << 32) + (i128)e.lo[j];
+      sums_out[a * D + j] = i128_to_double(v, -g.qexp[j]);
+    }
+    if (ncounts_out) {
+      u64 cnt;
+      i128 sum[D];
+      neighbourhood_sum<D>(g, tab, key, cnt, sum);
+      ncounts_out[a] = (i64)cnt;
+#pragma unroll
+      for (int j = 0; j < D; ++j) nsums_out[a * D + j] = i128_to_double(sum[j], -g.qexp[j]);
+    }
+  }
+}
+
+}  // namespace gs

@@ -1,0 +1,207 @@
+"""MeanShift++ engine surface of the reference (`gridshift/modeseek.py`),
+executed by the sm_100a kernels behind `libgridshift_cuda.so`.
+
+Drop-in: `meanshiftpp(PointSet, ShiftConfig) -> (Labeling, ShiftTrace)` has
+the reference signature (modeseek.py:125) and is what `ENGINES["meanshiftpp"]`
+holds (modeseek.py:288).  `install()` swaps it into an importable reference
+`gridshift` package so every caller there (segment_image, bench, CLI,
+tracker) runs on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .grid import PointSet, check_bandwidth
+
+_KERNELS = ("flat", "gaussian")
+DEFAULT_MAX_ITERS = 300      # modeseek.py:42
+ETA_SCALE = 1e-4             # modeseek.py:45
+
+
+@dataclass
+class ShiftConfig:
+    """modeseek.py:48-74 (kernel only matters for the quadratic baseline,
+    which this engine does not provide)."""
+
+    h: float
+    eta: float | None = None
+    max_iters: int = DEFAULT_MAX_ITERS
+    kernel: str = "flat"
+
+    def __post_init__(self):
+        check_bandwidth(self.h)
+        if self.eta is not None and (not np.isfinite(self.eta) or self.eta <= 0):
+            raise ValueError(f"eta must be positive and finite, got {self.eta}")
+        if int(self.max_iters) != self.max_iters or self.max_iters < 1:
+            raise ValueError(f"max_iters must be a positive integer, got {self.max_iters}")
+        if self.kernel not in _KERNELS:
+            raise ValueError(f"kernel must be one of {_KERNELS}, got {self.kernel!r}")
+
+    def resolve_eta(self, n: int) -> float:
+        return float(self.eta) if self.eta is not None else ETA_SCALE * n * self.h
+
+
+@dataclass
+class Labeling:
+    """modeseek.py:77-91."""
+
+    labels: np.ndarray
+    k: int
+    modes: np.ndarray
+
+    def __post_init__(self):
+        self.labels = np.ascontiguousarray(self.labels, dtype=np.int64)
+        self.modes = np.ascontiguousarray(self.modes, dtype=np.float64)
+        if self.k < 1 or self.modes.shape[0] != self.k:
+            raise ValueError(f"expected {self.k} mode rows, got {self.modes.shape}")
+        if self.labels.min() != 0 or self.labels.max() != self.k - 1:
+            raise ValueError("labels must cover [0, k) densely")
+
+
+@dataclass
+class ShiftTrace:
+    """modeseek.py:94-100, plus per-iteration occupied-cell counts and
+    (cells, counts) fingerprints recorded on device."""
+
+    iterations: int
+    total_movement_per_iter: np.ndarray = field(repr=False)
+    converged: bool = False
+    cells_per_iter: np.ndarray | None = field(default=None, repr=False)
+    fingerprint_per_iter: np.ndarray | None = field(default=None, repr=False)
+
+
+def _fetch(ctx, k: int, d: int, iters: int):
+    L = _lib.load()
+    modes = np.empty((k, d), dtype=np.float64)
+    _lib.check(L.gs_fetch_modes(ctx, _lib.ptr(modes), k))
+    kk = np.empty(iters, dtype=np.int64)
+    fp = np.empty(iters, dtype=np.uint64)
+    _lib.check(L.gs_fetch_trace(ctx, _lib.ptr(kk), _lib.ptr(fp), iters))
+    return modes, kk, fp
+
+
+def _finish(ctx, labels, k, d, iters, mv, conv):
+    modes, kk, fp = _fetch(ctx, k, d, iters)
+    lab = Labeling(labels=labels, k=k, modes=modes)
+    tr = ShiftTrace(iterations=iters, total_movement_per_iter=mv[:iters].copy(),
+                    converged=bool(conv), cells_per_iter=kk, fingerprint_per_iter=fp)
+    return lab, tr
+
+
+def meanshiftpp(points: PointSet, cfg: ShiftConfig) -> tuple[Labeling, ShiftTrace]:
+    """modeseek.py:125-146 on the B200: device-resident loop until the
+    summed movement drops below eta (the converging step applied) or
+    max_iters, then device-side cluster extraction."""
+    if not isinstance(points, PointSet):
+        points = PointSet(points)
+    L = _lib.load()
+    ctx = _lib.context()
+    y = points.data
+    n, d = y.shape
+    eta = cfg.resolve_eta(n)
+    labels = np.empty(n, dtype=np.int64)
+    mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
+    k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
+    _lib.check(L.gs_meanshiftpp(ctx, _lib.ptr(y), n, d, float(cfg.h), eta, int(cfg.max_iters),
+                                _lib.ptr(labels), _lib.ref(k), _lib.ref(it), _lib.ptr(mv),
+                                _lib.ref(conv)))
+    return _finish(ctx, labels, int(k.value), d, int(it.value), mv, conv.value)
+
+
+def meanshiftpp_device(x, cfg: ShiftConfig, labels_out=None, stream=None):
+    """Device-resident entry: `x` is a CUDA tensor (n, d) float64 or float32
+    (anything exposing data_ptr()).  Labels are written into `labels_out`
+    (CUDA int64 tensor, allocated if None).  Returns (labels_out, k, iters,
+    movement, converged); modes via `last_modes()`."""
+    import torch
+
+    L = _lib.load()
+    dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    ctx = _lib.context(dev)
+    n, d = x.shape
+    if not x.is_contiguous():
+        raise ValueError("device point data must be C-contiguous")
+    dtype = {torch.float64: _lib.GS_DTYPE_F64, torch.float32: _lib.GS_DTYPE_F32}.get(x.dtype)
+    if dtype is None:
+        raise ValueError("device point data must be float64 or float32")
+    if labels_out is None:
+        labels_out = torch.empty(n, dtype=torch.int64, device=x.device)
+    eta = cfg.resolve_eta(n)
+    mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
+    k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+    _lib.check(L.gs_meanshiftpp_device(ctx, C.c_void_p(x.data_ptr()), dtype, n, d, float(cfg.h),
+                                       eta, int(cfg.max_iters), C.c_void_p(labels_out.data_ptr()),
+                                       _lib.ref(k), _lib.ref(it), _lib.ptr(mv), _lib.ref(conv),
+                                       C.c_void_p(s)))
+    return labels_out, int(k.value), int(it.value), mv[: it.value].copy(), bool(conv.value)
+
+
+def last_modes(k: int, d: int, device: int | None = None) -> np.ndarray:
+    modes = np.empty((k, d), dtype=np.float64)
+    _lib.check(_lib.load().gs_fetch_modes(_lib.context(device), _lib.ptr(modes), k))
+    return modes
+
+
+def meanshiftpp_step(points: PointSet, cfg: ShiftConfig) -> tuple[PointSet, float]:
+    """modeseek.py:114-122: one grid-neighbourhood mean update on device."""
+    L = _lib.load()
+    ctx = _lib.context()
+    y = points.data
+    n, d = y.shape
+    out = np.empty_like(y)
+    mv = C.c_double(0.0)
+    _lib.check(L.gs_shift_step(ctx, _lib.ptr(y), n, d, float(cfg.h), _lib.ptr(out), _lib.ref(mv)))
+    return PointSet(out), float(mv.value)
+
+
+def extract_clusters(converged: PointSet, h: float) -> Labeling:
+    """modeseek.py:275-285 on device: bin at h, union-find over Chebyshev
+    adjacent occupied cells, first-appearance labels, mean modes."""
+    h = check_bandwidth(h)
+    L = _lib.load()
+    ctx = _lib.context()
+    y = converged.data
+    n, d = y.shape
+    labels = np.empty(n, dtype=np.int64)
+    k = C.c_int64(0)
+    _lib.check(L.gs_extract_clusters(ctx, _lib.ptr(y), n, d, h, _lib.ptr(labels), _lib.ref(k)))
+    modes = np.empty((int(k.value), d), dtype=np.float64)
+    _lib.check(L.gs_fetch_modes(ctx, _lib.ptr(modes), int(k.value)))
+    return Labeling(labels=labels, k=int(k.value), modes=modes)
+
+
+ENGINES = {"meanshiftpp": meanshiftpp}
+
+
+def install(gridshift_module=None) -> None:
+    """Register this engine in a reference `gridshift` installation:
+    ENGINES["meanshiftpp"] (modeseek.py:288) and the direct imports in
+    track.py:22 / bench.py:23 resolve to the CUDA engine.  The reference's
+    own PointSet/ShiftConfig objects are accepted (same fields)."""
+    import importlib
+
+    gs = gridshift_module or importlib.import_module("gridshift")
+    ms = importlib.import_module(gs.__name__ + ".modeseek")
+
+    def engine(points, cfg):
+        lab, tr = meanshiftpp(PointSet(points.data), ShiftConfig(cfg.h, cfg.eta, cfg.max_iters))
+        return (ms.Labeling(labels=lab.labels, k=lab.k, modes=lab.modes),
+                ms.ShiftTrace(iterations=tr.iterations,
+                              total_movement_per_iter=tr.total_movement_per_iter,
+                              converged=tr.converged))
+
+    ms.ENGINES["meanshiftpp"] = engine
+    ms.meanshiftpp = engine
+    for sub in ("track", "segment", "bench", "cli"):
+        try:
+            mod = importlib.import_module(gs.__name__ + "." + sub)
+        except ImportError:
+            continue
+        if hasattr(mod, "meanshiftpp"):
+            mod.meanshiftpp = engine

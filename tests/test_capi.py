@@ -1,0 +1,56 @@
+"""The C ABI library builds for sm_100a, loads without a GPU, and exports
+exactly the entry points include/gridshift_cuda.h declares."""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2104_00303_b200 import _build, _lib
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "gridshift_cuda.h"
+
+
+def declared():
+    txt = HEADER.read_text()
+    return sorted(set(re.findall(r"GS_API\s+[\w\s\*]+?\b(gs_\w+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return _lib.load()
+
+
+def test_header_declares_entry_points():
+    names = declared()
+    assert "gs_meanshiftpp" in names and "gs_track_sequence" in names
+    assert names == sorted(_lib.SIGNATURES), "ctypes table must mirror the header"
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(gs_\w+)", out))
+    assert exported == set(declared())
+    for name in declared():
+        assert isinstance(getattr(lib, name), ctypes._CFuncPtr)
+
+
+def test_version_and_error_strings(lib):
+    assert b"sm_100a" in lib.gs_version()
+    assert lib.gs_last_error() == b""
+
+
+def test_library_is_sm100a_code():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_null_context_is_rejected(lib):
+    rc = lib.gs_meanshiftpp(None, None, 1, 1, 1.0, 1.0, 1, None, None, None, None, None)
+    assert rc == _lib.GS_EINVAL

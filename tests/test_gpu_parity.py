@@ -1,0 +1,267 @@
+"""CUDA engine vs the reference (frozen fixtures) and the CPU oracle.
+
+Contract (BASELINE.json north_star): cell keys and per-cell counts
+bit-exact every iteration (checked through the order-independent
+(cells, counts) fingerprint the engine records on device), labels
+identical, modes within 1e-9*h in fp64.  Coordinate sums are exact on
+device and rounded once, the reference sums sequentially: the tolerance
+below is the reference's own (test_grid.py:116, rtol 1e-9).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2104_00303_b200 as gs
+from oracle import gridshift_oracle as O
+from paper_2104_00303_b200 import workloads as W
+from tests import goldens as G
+
+pytestmark = pytest.mark.gpu
+
+MODES_TOL = 1e-9   # * h
+
+
+def _eta(f):
+    return None if np.isnan(f["eta"]) else float(f["eta"])
+
+
+# ------------------------------------------------------------------ tables
+
+@pytest.mark.parametrize("c", G.cases("tables"))
+def test_tables_vs_reference(c):
+    f = G.case("tables", c)
+    t = gs.neighbor_stats(gs.PointSet(f["y"]), float(f["h"]))
+    assert np.array_equal(t.cells, f["cells"])
+    assert np.array_equal(t.counts, f["counts"])
+    np.testing.assert_allclose(t.sums, f["sums"], rtol=1e-12, atol=1e-300)
+    assert np.array_equal(t.nbr_counts, f["nbr_counts"])
+    scale = np.abs(f["y"]).max()
+    np.testing.assert_allclose(t.nbr_sums, f["nbr_sums"], rtol=1e-12, atol=1e-15 * scale * len(f["y"]))
+
+
+def test_tables_exact_sums():
+    # exact device sums == math.fsum of the member coordinates
+    rng = np.random.default_rng(5)
+    y = rng.uniform(1.0, 9.0, size=(5000, 3))
+    t = gs.build_cell_tables(gs.PointSet(y), 0.75)
+    cells = np.floor(y / 0.75).astype(np.int64)
+    for i in range(0, t.k, 7):
+        m = np.all(cells == t.cells[i], axis=1)
+        assert int(m.sum()) == int(t.counts[i])
+        want = [math.fsum(y[m, j]) for j in range(3)]
+        assert t.sums[i].tolist() == want
+
+
+# ------------------------------------------------------------------- steps
+
+@pytest.mark.parametrize("c", G.cases("steps"))
+def test_step_vs_reference(c):
+    # criterion 1 (test_acceptance.py:38-61): max error relative to the field
+    f = G.case("steps", c)
+    moved, mv = gs.meanshiftpp_step(gs.PointSet(f["y"]), gs.ShiftConfig(h=float(f["h"])))
+    want = f["y_next"]
+    rel = np.abs(moved.data - want).max() / max(np.abs(want).max(), 1e-30)
+    assert rel <= 1e-10
+    assert mv == pytest.approx(float(f["movement"]), rel=1e-9, abs=1e-12)
+
+
+def _exact_step(y, h):
+    cells = np.floor(y / h).astype(np.int64)
+    out = np.empty_like(y)
+    for i in range(len(y)):
+        near = np.abs(cells - cells[i]).max(axis=1) <= 1
+        cnt = int(near.sum())
+        out[i] = [math.fsum(y[near, j]) / cnt for j in range(y.shape[1])]
+    return out
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5])
+def test_step_is_exactly_rounded(d):
+    # values in [1, 2): fixed-point capture is exact, so the device result is
+    # the correctly rounded neighbourhood sum divided by the count
+    rng = np.random.default_rng(100 + d)
+    y = rng.uniform(1.0, 2.0, size=(300, d))
+    moved, _ = gs.meanshiftpp_step(gs.PointSet(y), gs.ShiftConfig(h=0.21))
+    assert np.array_equal(moved.data, _exact_step(y, 0.21))
+
+
+def test_step_kats():
+    # test_modeseek.py:92-105
+    pts = gs.PointSet(np.array([[3.7, -1.2]]))
+    moved, mv = gs.meanshiftpp_step(pts, gs.ShiftConfig(h=1.0))
+    assert np.array_equal(moved.data, pts.data) and mv == 0.0
+    moved, mv = gs.meanshiftpp_step(gs.PointSet(np.array([[0.1], [0.2]])), gs.ShiftConfig(h=1.0))
+    assert moved.data == pytest.approx(np.array([[0.15], [0.15]]), rel=1e-12)
+    assert mv == pytest.approx(0.1, rel=1e-12)
+
+
+# -------------------------------------------------------------------- runs
+
+def _mv_atol(n, scale):
+    # the reference's sequential fp64 sums carry O(cell size * eps) noise per
+    # point (visible once cells collapse); the device sums are exact
+    return max(n * scale * 1e-12, 1e-300)
+
+
+def _check_run(lab, tr, f, h, y=None):
+    assert tr.iterations == int(f["iterations"])
+    assert tr.converged == bool(f["converged"])
+    assert tr.cells_per_iter.tolist() == f["iter_k"].tolist()
+    assert [int(v) for v in tr.fingerprint_per_iter] == [int(v) for v in f["iter_fp"]]
+    n = int(f["n"]) if "n" in f else len(f["y"])
+    scale = float(np.abs(f["modes"]).max()) * 2 + h
+    np.testing.assert_allclose(tr.total_movement_per_iter, f["movement"], rtol=1e-9, atol=_mv_atol(n, scale))
+    assert lab.k == int(f["k"])
+    assert np.abs(lab.modes - f["modes"]).max() <= MODES_TOL * h
+
+
+@pytest.mark.parametrize("c", G.cases("runs"))
+def test_run_vs_reference(c):
+    f = G.case("runs", c)
+    h = float(f["h"])
+    lab, tr = gs.meanshiftpp(gs.PointSet(f["y"]), gs.ShiftConfig(h=h, eta=_eta(f), max_iters=int(f["max_iters"])))
+    assert np.array_equal(lab.labels, f["labels"])
+    _check_run(lab, tr, f, h)
+
+
+def test_run_kats():
+    # test_modeseek.py:141-236
+    lab, tr = gs.meanshiftpp(gs.PointSet(np.tile([1.5, -0.5, 2.0], (40, 1))), gs.ShiftConfig(h=0.7))
+    assert lab.k == 1 and np.all(lab.labels == 0) and tr.iterations == 1 and tr.converged
+    assert tr.total_movement_per_iter.sum() == 0.0
+    assert lab.modes[0].tolist() == [1.5, -0.5, 2.0]
+    lab, tr = gs.meanshiftpp(gs.PointSet(np.array([[0.2], [9.7]])), gs.ShiftConfig(h=1.0))
+    assert tr.iterations == 1 and tr.converged and tr.total_movement_per_iter[-1] == 0.0 and lab.k == 2
+    rng = np.random.default_rng(3)
+    data = rng.uniform(0, 1, size=(120, 3))
+    lab, tr = gs.meanshiftpp(gs.PointSet(data), gs.ShiftConfig(h=50.0))
+    assert lab.k == 1 and tr.converged
+    assert np.allclose(lab.modes[0], data.mean(axis=0), rtol=1e-9, atol=1e-12)
+
+
+def test_engine_is_deterministic():
+    # test_modeseek.py:229-236, on a large input where atomics interleave
+    y = W.cloud3d(400_000, seed=12).astype(np.float64)
+    cfg = gs.ShiftConfig(h=1.0, eta=1e-3, max_iters=20)
+    a, ta = gs.meanshiftpp(gs.PointSet(y), cfg)
+    b, tb = gs.meanshiftpp(gs.PointSet(y), cfg)
+    assert np.array_equal(a.labels, b.labels)
+    assert np.array_equal(a.modes, b.modes)
+    assert np.array_equal(ta.total_movement_per_iter, tb.total_movement_per_iter)
+
+
+def test_invalid_inputs_raise_value_error():
+    with pytest.raises(ValueError):
+        gs.ShiftConfig(h=0.0)
+    with pytest.raises(ValueError):
+        gs.PointSet(np.array([[1.0, np.nan]]))
+    with pytest.raises(ValueError):
+        gs.build_cell_tables(gs.PointSet(np.array([[1e30]])), 1e-8)
+    with pytest.raises(ValueError):
+        gs.meanshiftpp(gs.PointSet(np.array([[1e30]])), gs.ShiftConfig(h=1e-8))
+
+
+# -------------------------------------------------------------- extraction
+
+@pytest.mark.parametrize("c", G.cases("extract"))
+def test_extract_vs_reference(c):
+    f = G.case("extract", c)
+    lab = gs.extract_clusters(gs.PointSet(f["y"]), float(f["h"]))
+    assert lab.k == int(f["k"])
+    assert np.array_equal(lab.labels, f["labels"])
+    assert np.abs(lab.modes - f["modes"]).max() <= MODES_TOL * float(f["h"])
+
+
+# ---------------------------------------------------------------- tracking
+
+@pytest.mark.parametrize("c", G.cases("tracking"))
+def test_tracking_vs_reference(c):
+    f = G.case("tracking", c)
+    cx, cy, w, hp = f["win"].tolist()
+    win = gs.Window(cx=cx, cy=cy, w=int(w), h_px=int(hp))
+    rows = gs.track_sequence([gs.Image(p) for p in f["frames"]], win, gs.ShiftConfig(h=float(f["h"])),
+                             [int(f["selected"])], update_bins=bool(f["update"]))
+    assert [r.window.cx for r in rows] == f["cx"].tolist()
+    assert [r.window.cy for r in rows] == f["cy"].tolist()
+    assert [r.lost for r in rows] == f["lost"].tolist()
+    assert [r.last_match_count for r in rows] == f["matches"].tolist()
+    assert [len(r.bins.bins) for r in rows] == f["nbins"].tolist()
+    fps = [W.fingerprint(np.array(sorted(r.bins.bins), dtype=np.int64),
+                         np.zeros(len(r.bins.bins), dtype=np.int64)) for r in rows]
+    assert fps == [int(v) for v in f["bins_fp"]]
+
+
+def test_track_frame_matches_oracle():
+    f = G.case("tracking", "track_video_small")
+    frames = f["frames"]
+    cx, cy, w, hp = f["win"].tolist()
+    h = float(f["h"])
+    st = gs.init_tracker(gs.Image(frames[0]), gs.Window(cx, cy, int(w), int(hp)), gs.ShiftConfig(h=h),
+                         [int(f["selected"])])
+    ost = dict(cx=cx, cy=cy, w=int(w), hp=int(hp), bins=set(st.bins.bins), lost=False,
+               matches=st.last_match_count)
+    for t in range(1, 6):
+        st = gs.track_frame(st, gs.Image(frames[t]), gs.ShiftConfig(h=h), update_bins=True)
+        ost = O.track_frame(ost, frames[t], h, update_bins=True)
+        assert (st.window.cx, st.window.cy) == (ost["cx"], ost["cy"])
+        assert st.last_match_count == ost["matches"]
+        assert set(st.bins.bins) == ost["bins"]
+
+
+# ------------------------------------------------------------ segmentation
+
+def test_segment_fused_features_match_host_features():
+    img = gs.Image(W.voronoi_image(96, 64, 9, seed=21))
+    cfg = gs.ShiftConfig(h=10.0, eta=1e-3, max_iters=100)
+    seg, tr = gs.segment_image(img, cfg, mode="rgbxy", scale=0.25)
+    lab, tr2 = gs.meanshiftpp(gs.image_to_features(img, "rgbxy", scale=0.25), cfg)
+    assert np.array_equal(seg.labels.ravel(), lab.labels)
+    assert [int(v) for v in tr.fingerprint_per_iter] == [int(v) for v in tr2.fingerprint_per_iter]
+    r = O.meanshiftpp(O.image_to_features(img.pixels, "rgbxy", 0.25), 10.0, 1e-3, 100)
+    assert np.array_equal(lab.labels, r["labels"])
+
+
+# ------------------------------------------------------- full BASELINE sizes
+
+def test_cfg0_full_vs_reference():
+    f = G.big("cfg0")
+    c = W.CONFIGS["cfg0"]
+    lab, tr = gs.meanshiftpp(gs.PointSet(W.blobs2d()), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]))
+    assert np.array_equal(lab.labels, f["labels_u16"].astype(np.int64))
+    _check_run(lab, tr, f, c["h"])
+
+
+@pytest.mark.slow
+def test_cfg1_full_vs_reference():
+    f = G.big("cfg1")
+    c = W.CONFIGS["cfg1"]
+    img = gs.Image(W.cfg1_image())
+    lab, tr = gs.segment_pixels(img, gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]), "rgb")
+    assert np.array_equal(lab.labels, f["labels_u16"].astype(np.int64))
+    _check_run(lab, tr, f, c["h"])
+
+
+@pytest.mark.slow
+def test_cfg2_image_vs_reference():
+    f = G.big("cfg2")
+    c = W.CONFIGS["cfg2"]
+    img = gs.Image(W.cfg2_image(0))
+    lab, tr = gs.segment_pixels(img, gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]), "rgbxy", 0.25)
+    assert np.array_equal(lab.labels, f["labels_u16"].astype(np.int64))
+    _check_run(lab, tr, f, c["h"])
+
+
+@pytest.mark.slow
+def test_cfg4_10m_vs_reference():
+    import hashlib
+
+    f = G.big("cfg4_10m")
+    c = W.CONFIGS["cfg4"]
+    y = W.cloud3d(10_000_000).astype(np.float64)
+    lab, tr = gs.meanshiftpp(gs.PointSet(y), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]))
+    _check_run(lab, tr, f, c["h"])
+    a = np.ascontiguousarray(lab.labels)
+    dg = hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
+    assert dg == str(f["labels_digest"])
