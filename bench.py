@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""MeanShift++ grid shift on B200 -- benchmark (driver contract).
+
+One *step* = one full engine run (modeseek.py:125-146) over one batch of
+synthetic input: every grid-shift iteration to convergence / max_iter plus
+the device-side label extraction.  Metric: point-updates/s = points x
+iterations / seconds (BASELINE.json).  Workload: cfg4 (100M 3-D points,
+fp32 input upcast to fp64 iterates, h=1, tol=1e-3, max_iter=50), the largest
+configuration and the one the HBM-roofline and scaling targets are judged on.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 (torchrun, one rank per GPU): the 100M points are sharded by rows and
+the per-iteration cell tables are merged with an NCCL all-reduce (strong
+scaling, paper_2104_00303_b200/sharded.py).
+`--impl reference` times the reference algorithm's CPU restatement
+(oracle/, pinned to the reference's outputs) on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2104_00303_b200 import workloads as W  # noqa: E402
+
+METRIC = "point-updates/sec (points x iterations / s)"
+UNIT = "point-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=100_000_000, help="points (cfg4 default 1e8)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-kernels", action="store_true", default=True)
+    return ap.parse_args()
+
+
+def cfg4():
+    c = W.CONFIGS["cfg4"]
+    return c["h"], c["eta"], c["max_iters"]
+
+
+def workload_config(n, n_gpus):
+    h, eta, mi = cfg4()
+    return {"workload": f"cfg4: 3-D cloud, n={n:,} fp32 points (fp64 iterates), 50 rotated "
+                        f"anisotropic Gaussians + 10% uniform, h={h}, tol={eta}, max_iter={mi}",
+            "n": n, "d": 3, "h": h, "tol": eta, "max_iter": mi,
+            "sharding": "rows, per-iteration cell-table all-reduce" if n_gpus > 1 else "single GPU",
+            "l2": "inputs (1.2 GB fp32 + 2x2.4 GB fp64 iterates) exceed the 126 MB L2"}
+
+
+# ------------------------------------------------------------- clocks
+
+class Clocks:
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------- CPU baseline
+
+def cpu_sample(n_total, budget_s, x_host=None):
+    """Bounded sample of the same workload for the CPU restatement: the first
+    1,000,000 rows of the cfg4 input (rows are shuffled, so this is a uniform
+    random subsample) when the full input is at hand, else the cfg4 generator
+    at n=1,000,000; iteration cap sized to the time budget (~0.45 s/iter)."""
+    n = min(1_000_000, n_total)
+    iters = int(max(1, min(50, budget_s / 0.45)))
+    if x_host is not None:
+        return x_host[:n].astype(np.float64), iters, f"cfg4 input rows [0, {n:,})"
+    return W.cloud3d(n, seed=4).astype(np.float64), iters, f"cfg4 generator at n={n:,} (seed 4)"
+
+
+def run_oracle(x, iters):
+    from oracle import gridshift_oracle as O
+
+    h, eta, _ = cfg4()
+    t0 = time.perf_counter()
+    r = O.meanshiftpp(x, h, eta, iters)
+    dt = time.perf_counter() - t0
+    return x.shape[0] * r["iterations"], dt, r["iterations"]
+
+
+def reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    budget = max(5.0, 150.0 / max(1, a.steps + a.warmup))
+    x, iters, what = cpu_sample(a.n, budget)
+    for _ in range(a.warmup):
+        run_oracle(x, iters)
+    ups, secs = 0, 0.0
+    for _ in range(a.steps):
+        u, dt, _ = run_oracle(x, iters)
+        ups += u
+        secs += dt
+    v = ups / secs
+    sample = f"{what}, {iters} iterations per step (max_iter cap), h=1, tol=1e-3"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy, paper_2104_00303_b200/workloads.py)",
+            "config": workload_config(a.n, a.gpus),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
+                             "note": "numpy restatement of gridshift (oracle/), bitwise-pinned to the "
+                                     "reference's outputs; the reference path is single-threaded"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- our arm
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full summary."""
+    for f in sorted((ROOT / "profiles").glob("ncu_full_*.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+        except ValueError:
+            continue
+        k = d.get("kernels", {}).get(kernel)
+        if k and k.get("dram_bytes") is not None:
+            return float(k["dram_bytes"]), f.name
+    return None, None
+
+
+def our_arm(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_00303_b200 as gs
+    from paper_2104_00303_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ["GRIDSHIFT_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    h, eta, mi = cfg4()
+    n = a.n
+    x_host = W.cloud3d(n)                       # fp32 (n, 3), seeded
+    if world > 1:
+        from paper_2104_00303_b200 import sharded
+
+        lo, hi = sharded.shard_bounds(n, world, rank)
+        x_dev = torch.from_numpy(x_host[lo:hi]).cuda()
+    else:
+        x_dev = torch.from_numpy(x_host).cuda()
+    cfg = gs.ShiftConfig(h=h, eta=eta, max_iters=mi)
+    labels = torch.empty(x_dev.shape[0], dtype=torch.int64, device="cuda")
+
+    def step():
+        if world > 1:
+            return sharded.meanshiftpp_sharded(x_dev, cfg, labels, n_total=n)
+        _, k, it, mv, conv = gs.meanshiftpp_device(x_dev, cfg, labels)
+        return it
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    _lib.profile(1)
+    iters_total = 0
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            iters_total += step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    prof = _lib.profile(2)
+    _lib.profile(0)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    per_step_iters = iters_total / a.steps
+    value = n * iters_total / (ms / 1e3)
+
+    # roofline of the dominant per-point kernel
+    n_local = x_dev.shape[0]
+    d = 3
+    bytes_per = {"hist": 8 * d * n_local, "shift": 16 * d * n_local}
+    work = {"hist": iters_total + a.steps, "shift": iters_total}   # +1 extraction hist per step
+    kern = max(("hist", "shift", "agg"), key=lambda k: prof[k][0])
+    peak, peak_src = measured_peak()
+    roof = None
+    if kern in bytes_per:
+        alg = bytes_per[kern] * work[kern]
+        achieved = alg / (prof[kern][0] / 1e3) / 1e9
+        traffic, tsrc = ncu_traffic(kern)
+        roof = {"kernel": f"k_{kern}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": bytes_per[kern],
+                "avg_launch_ms": prof[kern][0] / work[kern], "traffic_source": tsrc}
+    kernels = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
+    for k in ("hist", "shift"):
+        if k in kernels and prof[k][0] > 0:
+            kernels[k]["achieved_gbs"] = bytes_per[k] * work[k] / (prof[k][0] / 1e3) / 1e9
+    launches = int(sum(v[1] for v in prof.values()))
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": max(3, a.warmup), "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy, paper_2104_00303_b200/workloads.py); fp32 input upcast "
+                    "on device like PointSet (grid.py:43)",
+            "config": workload_config(n, world), "iterations_per_step": per_step_iters,
+            "roofline": roof, "kernels": kernels, "gpu_launches": launches,
+            "clocks": clk.summary()}
+
+    if rank == 0 and world == 1 and not a.no_e2e:
+        line["e2e"] = e2e(x_host, cfg, n, min(a.steps, 3))
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        x, iters, what = cpu_sample(n, 12.0, x_host)
+        ups, secs, it = run_oracle(x, iters)
+        line["cpu_baseline"] = {"value": ups / secs, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"{what} (uniform random subsample), {it} iterations, "
+                                          f"oracle/gridshift_oracle.py (numpy, single-threaded)"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def e2e(x_host, cfg, n, steps):
+    """Public host API (meanshiftpp(PointSet, ShiftConfig)) with the input in
+    pinned host memory: H2D of the points and D2H of labels + modes inside
+    the timed region, every step."""
+    import torch
+
+    import paper_2104_00303_b200 as gs
+
+    pts = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
+    pts[:] = x_host
+    lab_out = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+    P = gs.PointSet(pts)
+    gs.meanshiftpp(P, cfg, labels_out=lab_out)     # warm
+    ups = 0
+    k = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        lab, tr = gs.meanshiftpp(P, cfg, labels_out=lab_out)
+        ups += n * tr.iterations
+        k = lab.k
+    dt = time.perf_counter() - t0
+    return {"value": ups / dt, "unit": UNIT, "h2d_bytes_per_step": int(pts.nbytes),
+            "d2h_bytes_per_step": int(lab_out.nbytes + k * 3 * 8), "steps": steps,
+            "api": "paper_2104_00303_b200.meanshiftpp(PointSet, ShiftConfig) -> gs_meanshiftpp (C ABI)"}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        reference_arm(a)
+    else:
+        our_arm(a)
+
+
+if __name__ == "__main__":
+    main()

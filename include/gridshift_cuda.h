@@ -108,6 +108,13 @@ GS_API int gs_fetch_modes(gs_ctx* ctx, double* modes_out, int64_t cap_rows);
  * last run (observability; pins per-iteration tables bit for bit). */
 GS_API int gs_fetch_trace(gs_ctx* ctx, int64_t* k_per_iter, uint64_t* fp_per_iter, int32_t cap);
 
+/* Kernel accounting.  mode 1: enable per-launch CUDA-event timing (and
+ * reset counters); mode 0: disable (and reset); mode 2: write the
+ * accumulated device milliseconds and launch counts per kernel kind
+ * (index -> name via gs_profile_kind) into ms_out / launches_out[cap]. */
+GS_API int gs_profile(gs_ctx* ctx, int32_t mode, double* ms_out, int64_t* launches_out, int32_t cap);
+GS_API const char* gs_profile_kind(int32_t kind);
+
 /* One grid-mean update: replaces meanshiftpp_step (modeseek.py:114-122). */
 GS_API int gs_shift_step(gs_ctx* ctx, const double* y, int64_t n, int32_t d, double h, double* y_out,
                   double* movement_out);

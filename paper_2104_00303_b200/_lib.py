@@ -38,11 +38,13 @@ SIGNATURES = {
                                    _P, _P]),
     "gs_fetch_modes": (C.c_int, [_P, _P, _i64]),
     "gs_fetch_trace": (C.c_int, [_P, _P, _P, _i32]),
+    "gs_profile": (C.c_int, [_P, _i32, _P, _P, _i32]),
+    "gs_profile_kind": (C.c_char_p, [_i32]),
     "gs_shift_step": (C.c_int, [_P, _P, _i64, _i32, _f64, _P, _P]),
     "gs_build_tables": (C.c_int, [_P, _P, _i64, _i32, _f64, _i64, _P, _P, _P, _P, _P, _P]),
     "gs_extract_clusters": (C.c_int, [_P, _P, _i64, _i32, _f64, _P, _P]),
     "gs_track_sequence": (C.c_int, [_P, _P, _i32, _i32, _i32, _f64, _f64, _i32, _i32, _P, _i32,
-                                    _f64, _i32, _i32, _f64, _i32, _P, _P, _P, _P, _P, _P, _P]),
+                                    _f64, _i32, _i32, _f64, _i32, _P, _P, _P, _P, _P, _P]),
     "gs_fetch_track_bins": (C.c_int, [_P, _P, _i32, _P]),
 }
 
@@ -107,3 +109,17 @@ def ptr(a: np.ndarray | None):
 
 def ref(x):
     return C.byref(x)
+
+
+N_KINDS = 11
+
+
+def profile(mode: int, device: int | None = None):
+    """Kernel accounting of this thread's context (see gs_profile)."""
+    ms = np.zeros(N_KINDS)
+    cnt = np.zeros(N_KINDS, dtype=np.int64)
+    check(load().gs_profile(context(device), mode, ptr(ms), ptr(cnt), N_KINDS))
+    if mode != 2:
+        return None
+    names = [load().gs_profile_kind(i).decode() for i in range(N_KINDS)]
+    return {nm: (float(ms[i]), int(cnt[i])) for i, nm in enumerate(names)}

@@ -45,6 +45,7 @@ struct GridParams {
   int qexp[GS_MAXD];       // s_j
   u64 nkeys;               // prod of extents
   u64 mask;                // hash mask (cap - 1) or 0 for dense tables
+  i64 ld;                  // SoA leading dimension of the iterate (n rounded up to 64)
 };
 
 // Device-resident loop control.  One per context.

@@ -46,6 +46,25 @@ struct Buf {
   size_t cap = 0;
 };
 
+enum Kind { K_INIT = 0, K_HIST, K_AGG, K_SHIFT, K_CLEAR, K_COMP, K_LABELS, K_XPOSE, K_DUMP, K_TRACK,
+            K_SORT, K_NKINDS };
+const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "shift", "clear", "components",
+                                          "labels", "transpose", "dump", "track", "sort"};
+
+constexpr int64_t kSortMinPoints = 1 << 15;   // spatial sort pays off above this
+
+inline int64_t soa_ld(int64_t n) { return (n + 63) & ~int64_t(63); }
+
+// Per-context kernel accounting: every launch is counted; with profiling on,
+// each launch is bracketed by CUDA events on the launching stream.
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, size_t>> rec;   // (kind, first event index)
+  int64_t launches[K_NKINDS] = {};
+};
+
 }  // namespace
 
 struct gs_ctx {
@@ -57,7 +76,7 @@ struct gs_ctx {
   // device buffers
   Buf x_stage, y[2], ent[2], keys[2], list[2], targets, partials, par, first, aux, roots,
       root_first, ranks, modes, labels, mv_hist, fp_hist, k_hist, stats, ctrl, perm, track,
-      track_out, bitmaps;
+      track_out, bitmaps, scan;
   // pinned host mirrors
   Ctrl* h_ctrl = nullptr;
   InitStats* h_stats = nullptr;
@@ -69,6 +88,7 @@ struct gs_ctx {
   std::vector<int64_t> iter_k;
   std::vector<uint64_t> iter_fp;
   std::vector<int64_t> track_bins;
+  Prof prof;
 };
 
 namespace {
@@ -86,6 +106,29 @@ T* ensure(gs_ctx* c, Buf& b, size_t count, int fill = 0) {
     b.cap = alloc;
   }
   return static_cast<T*>(b.p);
+}
+
+cudaEvent_t prof_event(gs_ctx* c) {
+  if (c->prof.used == c->prof.pool.size()) {
+    cudaEvent_t e;
+    GS_CUDA(cudaEventCreate(&e));
+    c->prof.pool.push_back(e);
+  }
+  return c->prof.pool[c->prof.used++];
+}
+
+template <typename F>
+void launch(gs_ctx* c, int kind, F&& f) {
+  c->prof.launches[kind] += 1;
+  if (!c->prof.on) {
+    f();
+    return;
+  }
+  const size_t i0 = c->prof.used;
+  GS_CUDA(cudaEventRecord(prof_event(c), c->st));
+  f();
+  GS_CUDA(cudaEventRecord(prof_event(c), c->st));
+  c->prof.rec.emplace_back(kind, i0);
 }
 
 inline int blocks_for(gs_ctx* c, int64_t work, int per_sm = 8) {
@@ -161,6 +204,7 @@ Plan make_plan(int64_t n, int d, double h, const InitStats& s) {
     acc *= (uint64_t)ext[j];
   }
   g.nkeys = acc;
+  g.ld = soa_ld(n);
   int em = 0;
   frexp(std::sqrt(span2) * 1.0000001 + 1e-300, &em);
   g.movement_exp = em;
@@ -249,12 +293,12 @@ InitStats run_init(gs_ctx* c, const Input& in, int64_t n, double h, double* y0) 
   GS_CUDA(cudaMemcpyAsync(dst, c->h_stats, sizeof hs, cudaMemcpyHostToDevice, c->st));
   const int nb = blocks_for(c, n);
   if (in.kind == IN_F64)
-    k_init_aos<D, double><<<nb, kThreads, 0, c->st>>>((const double*)in.dev, y0, n, h, dst);
+    launch(c, K_INIT, [&] { k_init_aos<D, double><<<nb, kThreads, 0, c->st>>>((const double*)in.dev, y0, n, soa_ld(n), h, dst); });
   else if (in.kind == IN_F32)
-    k_init_aos<D, float><<<nb, kThreads, 0, c->st>>>((const float*)in.dev, y0, n, h, dst);
+    launch(c, K_INIT, [&] { k_init_aos<D, float><<<nb, kThreads, 0, c->st>>>((const float*)in.dev, y0, n, soa_ld(n), h, dst); });
   else {
     if constexpr (D == 3 || D == 5)
-      k_init_image<D><<<nb, kThreads, 0, c->st>>>((const unsigned char*)in.dev, y0, n, in.width, in.scale, h, dst);
+      launch(c, K_INIT, [&] { k_init_image<D><<<nb, kThreads, 0, c->st>>>((const unsigned char*)in.dev, y0, n, soa_ld(n), in.width, in.scale, h, dst); });
   }
   check_launch();
   GS_CUDA(cudaMemcpyAsync(c->h_stats, dst, sizeof hs, cudaMemcpyDeviceToHost, c->st));
@@ -271,40 +315,40 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
   double* y_in = static_cast<double*>(c->y[cur].p);
   double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
-  k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, n, p.g, tabs[cur], ctrl, 1);
-  k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1],
+  launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, n, p.g, tabs[cur], ctrl, 1); });
+  launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1],
                                                   static_cast<double*>(c->targets.p), ctrl, cur,
                                                   static_cast<u64*>(c->fp_hist.p) + t,
-                                                  static_cast<u32*>(c->k_hist.p) + t);
-  k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur],
+                                                  static_cast<u32*>(c->k_hist.p) + t); });
+  launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur],
                                                   static_cast<const double*>(c->targets.p), ctrl,
                                                   static_cast<u64*>(c->partials.p),
-                                                  static_cast<double*>(c->mv_hist.p), t, eta, cur);
+                                                  static_cast<double*>(c->mv_hist.p), t, eta, cur); });
 }
 
 // Extraction of y_final (modeseek.py:256-272).  Table buffer e is clean on
 // entry, buffer e^1 is dirty (cleared here and used as component scratch).
 template <int D, class Tab>
 void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
-                 int64_t* labels_dev) {
+                 int64_t* labels_dev, const u32* perm = nullptr) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
-  k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e ^ 1], &ctrl->k[e ^ 1]);
-  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e ^ 1]);
-  k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], ctrl, 0);
+  launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e ^ 1], &ctrl->k[e ^ 1]); });
+  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e ^ 1]); });
+  launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], ctrl, 0); });
   u32* par = ensure<u32>(c, c->par, p.slots);
   u32* first = ensure<u32>(c, c->first, p.slots);
   u32* rankmap = ensure<u32>(c, c->aux, p.slots);
   u32* roots = ensure<u32>(c, c->roots, p.list_cap + 1);
   u32* rfirst = ensure<u32>(c, c->root_first, p.list_cap + 1);
   u32* nroots = ensure<u32>(c, c->partials, 2 * (size_t)c->sms * 8 + 2);  // reuse scratch
-  k_uf_init<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first);
-  k_uf_link<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[e], &ctrl->k[e], par);
-  k_uf_flatten<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, tabs[e ^ 1].ent);
-  k_first<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, first, nullptr, ctrl);
+  launch(c, K_COMP, [&] { k_uf_init<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first); });
+  launch(c, K_COMP, [&] { k_uf_link<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[e], &ctrl->k[e], par); });
+  launch(c, K_COMP, [&] { k_uf_flatten<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, tabs[e ^ 1].ent); });
+  launch(c, K_LABELS, [&] { k_first<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, first, perm, ctrl); });
   GS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(u32), c->st));
-  k_roots<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first, roots, rfirst, nroots);
+  launch(c, K_COMP, [&] { k_roots<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first, roots, rfirst, nroots); });
   check_launch();
   u32 nr = 0;
   GS_CUDA(cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->st));
@@ -326,17 +370,43 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
   u32* dranks = ensure<u32>(c, c->ranks, nr + 1);
   GS_CUDA(cudaMemcpyAsync(dranks, rk.data(), nr * sizeof(u32), cudaMemcpyHostToDevice, c->st));
   double* dmodes = ensure<double>(c, c->modes, (size_t)nr * D + 1);
-  k_modes<D><<<blocks_for(c, nr), kThreads, 0, c->st>>>(p.g, roots, dranks, nr, rankmap, tabs[e ^ 1].ent, dmodes);
-  k_labels<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, rankmap, nullptr,
-                                                   reinterpret_cast<i64*>(labels_dev));
-  k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e]);
-  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e]);
+  launch(c, K_COMP, [&] { k_modes<D><<<blocks_for(c, nr), kThreads, 0, c->st>>>(p.g, roots, dranks, nr, rankmap, tabs[e ^ 1].ent, dmodes); });
+  launch(c, K_LABELS, [&] { k_labels<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, rankmap, perm,
+                                                   reinterpret_cast<i64*>(labels_dev)); });
+  launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e]); });
+  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e]); });
   check_launch();
   c->modes_host.resize((size_t)nr * D);
   GS_CUDA(cudaMemcpyAsync(c->modes_host.data(), dmodes, (size_t)nr * D * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   sync(c);
   c->k_last = nr;
   c->d_last = D;
+}
+
+// One-time counting sort of the iterate by initial cell (see k_scatter).
+// Leaves table buffer 0 clean; y[0] holds the sorted iterate afterwards and
+// the returned perm maps sorted position -> original point index.
+template <int D, class Tab>
+const u32* spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  const int nb_pts = blocks_for(c, n);
+  const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
+  const int nbs = (int)((p.list_cap + kScanChunk - 1) / kScanChunk);
+  u64* bsum = ensure<u64>(c, c->scan, (size_t)nbs + 1);
+  u32* off = ensure<u32>(c, c->aux, p.slots);
+  u32* perm = ensure<u32>(c, c->perm, (size_t)n);
+  double* y0 = static_cast<double*>(c->y[0].p);
+  double* y1 = static_cast<double*>(c->y[1].p);
+  launch(c, K_SORT, [&] { k_hist<D, Tab, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
+  launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, tabs[0].list, &ctrl->k[0], bsum); });
+  launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
+  launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, tabs[0].list, &ctrl->k[0], bsum, off); });
+  launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, y1, n, p.g, tabs[0], off, perm, ctrl); });
+  launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[0], &ctrl->k[0]); });
+  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]); });
+  check_launch();
+  std::swap(c->y[0], c->y[1]);
+  return perm;
 }
 
 struct RunOut {
@@ -348,8 +418,8 @@ struct RunOut {
 template <int D>
 RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta, int max_iters,
                     int64_t* labels_dev, double* movement_out) {
-  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
-  ensure<double>(c, c->y[1], (size_t)n * D);
+  double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n) * D);
+  ensure<double>(c, c->y[1], (size_t)soa_ld(n) * D);
   ensure<Ctrl>(c, c->ctrl, 1);
   const InitStats s = run_init<D>(c, in, n, h, y0);
   Plan p = make_plan(n, D, h, s);
@@ -363,6 +433,9 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   ensure<u32>(c, c->k_hist, (size_t)max_iters);
   GS_CUDA(cudaMemsetAsync(fp, 0, sizeof(u64) * max_iters, c->st));
   reset_ctrl(c);
+  const u32* perm = nullptr;
+  if (n >= kSortMinPoints)
+    perm = p.dense ? spatial_sort<D>(c, p, tabs.dn, n) : spatial_sort<D>(c, p, tabs.hs, n);
   // device-driven loop: enqueue chunks, synchronise between chunks only
   int t = 0, chunk = 4;
   while (t < max_iters) {
@@ -385,9 +458,9 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   const int e = r.iters & 1;
   const double* yf = static_cast<const double*>(c->y[e].p);
   if (p.dense)
-    run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev);
+    run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev, perm);
   else
-    run_extract<D>(c, p, tabs.hs, yf, n, e, labels_dev);
+    run_extract<D>(c, p, tabs.hs, yf, n, e, labels_dev, perm);
   r.k = c->k_last;
   if (movement_out)
     GS_CUDA(cudaMemcpyAsync(movement_out, c->mv_hist.p, sizeof(double) * r.iters, cudaMemcpyDeviceToHost, c->st));
@@ -423,8 +496,8 @@ void validate_run(int64_t n, int d, double h, double eta, int max_iters) {
 
 template <int D>
 void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_out_host, double* movement) {
-  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
-  double* y1 = ensure<double>(c, c->y[1], (size_t)n * D);
+  double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n) * D);
+  double* y1 = ensure<double>(c, c->y[1], (size_t)soa_ld(n) * D);
   ensure<Ctrl>(c, c->ctrl, 1);
   Input in{IN_F64, xdev};
   const InitStats s = run_init<D>(c, in, n, h, y0);
@@ -441,14 +514,14 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   if (p.dense) {
     enqueue_iteration<D>(c, p, tabs.dn, 0, -1.0, n, nb_pts, nb_cells);
-    k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.dn[0], &ctrl->k[0]);
+    launch(c, K_CLEAR, [&] { k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.dn[0], &ctrl->k[0]); });
   } else {
     enqueue_iteration<D>(c, p, tabs.hs, 0, -1.0, n, nb_pts, nb_cells);
-    k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.hs[0], &ctrl->k[0]);
+    launch(c, K_CLEAR, [&] { k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.hs[0], &ctrl->k[0]); });
   }
-  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]);
+  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]); });
   double* aos = ensure<double>(c, c->x_stage, (size_t)n * D);
-  k_soa_to_aos<D><<<nb_pts, kThreads, 0, c->st>>>(y1, aos, n);
+  launch(c, K_XPOSE, [&] { k_soa_to_aos<D><<<nb_pts, kThreads, 0, c->st>>>(y1, aos, n, p.g.ld); });
   check_launch();
   read_ctrl(c);
   check_flags(c->h_ctrl->error);
@@ -474,7 +547,7 @@ int64_t dump_tables(gs_ctx* c, const Plan& p, Tab* tabs, int64_t cap, int64_t* c
       dnc = ensure<i64>(c, c->ranks, k);
       dns = ensure<double>(c, c->aux, (size_t)k * D);
     }
-    k_dump<D, Tab><<<blocks_for(c, k), kThreads, 0, c->st>>>(p.g, tabs[0], &ctrl->k[0], dk, dc, ds, dnc, dns);
+    launch(c, K_DUMP, [&] { k_dump<D, Tab><<<blocks_for(c, k), kThreads, 0, c->st>>>(p.g, tabs[0], &ctrl->k[0], dk, dc, ds, dnc, dns); });
     check_launch();
     std::vector<u64> hk(k);
     std::vector<i64> hc(k), hnc(nc_out ? k : 0);
@@ -502,8 +575,8 @@ int64_t dump_tables(gs_ctx* c, const Plan& p, Tab* tabs, int64_t cap, int64_t* c
       if (nc_out) nc_out[r] = hnc[a];
     }
   }
-  k_clear<D, Tab><<<blocks_for(c, (int64_t)p.list_cap), kThreads, 0, c->st>>>(tabs[0], &ctrl->k[0]);
-  k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]);
+  launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<blocks_for(c, (int64_t)p.list_cap), kThreads, 0, c->st>>>(tabs[0], &ctrl->k[0]); });
+  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]); });
   check_launch();
   sync(c);
   return k;
@@ -512,7 +585,7 @@ int64_t dump_tables(gs_ctx* c, const Plan& p, Tab* tabs, int64_t cap, int64_t* c
 template <int D>
 int64_t run_tables_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t cap, int64_t* cells,
                      int64_t* counts, double* sums, int64_t* nc, double* ns) {
-  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
+  double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n) * D);
   ensure<Ctrl>(c, c->ctrl, 1);
   Input in{IN_F64, xdev};
   const InitStats s = run_init<D>(c, in, n, h, y0);
@@ -522,16 +595,16 @@ int64_t run_tables_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   if (p.dense) {
-    k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.dn[0], ctrl, 0);
+    launch(c, K_HIST, [&] { k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.dn[0], ctrl, 0); });
     return dump_tables<D>(c, p, tabs.dn, cap, cells, counts, sums, nc, ns);
   }
-  k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.hs[0], ctrl, 0);
+  launch(c, K_HIST, [&] { k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.hs[0], ctrl, 0); });
   return dump_tables<D>(c, p, tabs.hs, cap, cells, counts, sums, nc, ns);
 }
 
 template <int D>
 int64_t run_extract_only_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t* labels_dev) {
-  double* y0 = ensure<double>(c, c->y[0], (size_t)n * D);
+  double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n) * D);
   ensure<Ctrl>(c, c->ctrl, 1);
   Input in{IN_F64, xdev};
   const InitStats s = run_init<D>(c, in, n, h, y0);
@@ -617,12 +690,13 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->list[0], &c->list[1], &c->targets, &c->partials, &c->par, &c->first, &c->aux,
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
-                 &c->track_out, &c->bitmaps};
+                 &c->track_out, &c->bitmaps, &c->scan};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->h_small) cudaFreeHost(c->h_small);
+  for (cudaEvent_t e : c->prof.pool) cudaEventDestroy(e);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -690,6 +764,34 @@ int gs_fetch_modes(gs_ctx* c, double* modes_out, int64_t cap_rows) {
     if (cap_rows < c->k_last) fail(GS_EINVAL, "modes buffer too small");
     memcpy(modes_out, c->modes_host.data(), sizeof(double) * c->modes_host.size());
   });
+}
+
+int gs_profile(gs_ctx* c, int32_t mode, double* ms_out, int64_t* launches_out, int32_t cap) {
+  return guarded(c, [&] {
+    if (mode == 1 || mode == 0) {  // enable / disable, resetting the counters
+      c->prof.on = (mode == 1);
+      c->prof.used = 0;
+      c->prof.rec.clear();
+      for (auto& l : c->prof.launches) l = 0;
+      return;
+    }
+    // mode 2: fetch accumulated per-kind device time (ms) and launch counts
+    sync(c);
+    double ms[K_NKINDS] = {};
+    for (auto& r : c->prof.rec) {
+      float t = 0.f;
+      GS_CUDA(cudaEventElapsedTime(&t, c->prof.pool[r.second], c->prof.pool[r.second + 1]));
+      ms[r.first] += t;
+    }
+    for (int k = 0; k < K_NKINDS && k < cap; ++k) {
+      if (ms_out) ms_out[k] = ms[k];
+      if (launches_out) launches_out[k] = c->prof.launches[k];
+    }
+  });
+}
+
+const char* gs_profile_kind(int32_t kind) {
+  return (kind >= 0 && kind < K_NKINDS) ? kKindNames[kind] : "";
 }
 
 int gs_fetch_trace(gs_ctx* c, int64_t* k_per_iter, uint64_t* fp_per_iter, int32_t cap) {
@@ -823,8 +925,8 @@ int gs_track_sequence(gs_ctx* c, const uint8_t* frames, int32_t n_frames, int32_
     tp.cy0 = cy;
     tp.words = words;
     tp.init_matches = init_matches;
-    k_track<<<1, kTrackThreads, 0, c->st>>>(df, tp, dlut, dbm, dbm + words, dcx, dcy, dlost, dm, dnb,
-                                            dhist);
+    launch(c, K_TRACK, [&] { k_track<<<1, kTrackThreads, 0, c->st>>>(df, tp, dlut, dbm, dbm + words, dcx, dcy, dlost, dm, dnb,
+                                            dhist); });
     check_launch();
     GS_CUDA(cudaMemcpyAsync(cx_out, dcx, 8 * T, cudaMemcpyDeviceToHost, c->st));
     GS_CUDA(cudaMemcpyAsync(cy_out, dcy, 8 * T, cudaMemcpyDeviceToHost, c->st));

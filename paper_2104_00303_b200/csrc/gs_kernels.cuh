@@ -151,7 +151,7 @@ struct InitStats {
 
 template <int D, typename T>
 __global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, double* __restrict__ y,
-                                                       i64 n, double h, InitStats* st) {
+                                                       i64 n, i64 ld, double h, InitStats* st) {
   i64 cmin[D], cmax[D];
   u64 amax[D];
 #pragma unroll
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, 
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const double v = (double)x[i * D + j];
-      y[(i64)j * n + i] = v;
+      y[(i64)j * ld + i] = v;
       if (!isfinite(v)) { flags |= kErrNonFinite; continue; }
       const double c = cell_of(v, h);
       if (fabs(c) >= 4611686018427387904.0) { flags |= kErrLattice; continue; }
@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, 
 // uint8 image (H, W, 3) -> rgb or rgbxy features (segment.py:82-92), fused.
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_init_image(const unsigned char* __restrict__ px, double* __restrict__ y,
-                                                         i64 n, int width, double scale, double h, InitStats* st) {
+                                                         i64 n, i64 ld, int width, double scale, double h,
+                                                         InitStats* st) {
   i64 cmin[D], cmax[D];
   u64 amax[D];
 #pragma unroll
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_init_image(const unsigned char* __
     }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      y[(i64)j * n + i] = v[j];
+      y[(i64)j * ld + i] = v[j];
       const i64 ci = (i64)cell_of(v[j], h);
       cmin[j] = min(cmin[j], ci);
       cmax[j] = max(cmax[j], ci);
@@ -241,17 +242,17 @@ __global__ void __launch_bounds__(kThreads) k_init_image(const unsigned char* __
 
 // SoA fp64 -> AoS fp64 (meanshiftpp_step output).
 template <int D>
-__global__ void k_soa_to_aos(const double* __restrict__ y, double* __restrict__ x, i64 n) {
+__global__ void k_soa_to_aos(const double* __restrict__ y, double* __restrict__ x, i64 n, i64 ld) {
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) x[i * D + j] = y[(i64)j * n + i];
+    for (int j = 0; j < D; ++j) x[i * D + j] = y[(i64)j * ld + i];
   }
 }
 
 // --------------------------------------------------------------- k_hist
 
-template <int D, class Tab>
+template <int D, class Tab, bool CountOnly = false>
 __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y, i64 n, GridParams g,
                                                    Tab tab, Ctrl* ctrl, int check_done) {
   if (check_done && *(volatile int*)&ctrl->done) return;
@@ -267,12 +268,14 @@ __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y,
     if (i < n) {
       double v[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * n + i);
+      for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * g.ld + i);
       bool inside;
       key = pack_key<D>(g, v, inside);
       if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+      if constexpr (!CountOnly) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) fx[j] = to_fixed(v[j], g.qscale[j]);
+        for (int j = 0; j < D; ++j) fx[j] = to_fixed(v[j], g.qscale[j]);
+      }
     }
     // segments: maximal runs of consecutive lanes with the same key
     const u64 pkey = __shfl_up_sync(kFull, key, 1);
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y,
 #pragma unroll
     for (int j = 0; j < D; ++j) same_val &= ((i64)__shfl_up_sync(kFull, (unsigned long long)fx[j], 1) == fx[j]);
     const u32 heads = __ballot_sync(kFull, !same_prev);
-    const u32 mixed = __ballot_sync(kFull, same_prev && !same_val);
+    const u32 mixed = CountOnly ? 0u : __ballot_sync(kFull, same_prev && !same_val);
     const u32 after = (lane == 31) ? 0u : (heads & (~0u << (lane + 1)));
     const int end = after ? (__ffs(after) - 1) : 32;
     i64 shi[D];
@@ -318,10 +321,12 @@ __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y,
         Entry<D>* e = tab.ent + s;
         const u64 old = atomicAdd(&e->count, cnt);
         if (Tab::kDense ? (old == 0) : fresh) tab.list[atomicAdd(tab.k, 1u)] = s;
+        if constexpr (!CountOnly) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          atomicAdd(&e->hi[j], (u64)shi[j]);
-          atomicAdd(&e->lo[j], slo[j]);
+          for (int j = 0; j < D; ++j) {
+            atomicAdd(&e->hi[j], (u64)shi[j]);
+            atomicAdd(&e->lo[j], slo[j]);
+          }
         }
       }
     }
@@ -393,6 +398,31 @@ __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab pre
 // -------------------------------------------------------------- k_shift
 
 template <int D, class Tab>
+__device__ __forceinline__ double shift_point(const GridParams& g, const Tab& tab,
+                                              const double* __restrict__ targets, const double* v,
+                                              double* out, Ctrl* ctrl) {
+  bool inside;
+  const u64 key = pack_key<D>(g, v, inside);
+  u32 s;
+  if constexpr (Tab::kDense) {
+    s = (u32)key;
+    if (!inside) { atomicOr(&ctrl->error, kErrMissing); s = 0; }
+  } else {
+    if (!inside || !tab.find(key, s)) { atomicOr(&ctrl->error, kErrMissing); s = 0; }
+  }
+  double sq[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    out[j] = __ldg(targets + (i64)s * D + j);
+    const double dlt = __dsub_rn(out[j], v[j]);
+    sq[j] = __dmul_rn(dlt, dlt);
+  }
+  return __dsqrt_rn(row_sum<D>(sq));
+}
+
+// Two consecutive points per thread and loop trip (16-byte vector loads of
+// each SoA axis); streaming loads/stores keep the cell tables in L2.
+template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
                                                     GridParams g, Tab tab, const double* __restrict__ targets,
                                                     Ctrl* ctrl, u64* partials, double* mv_hist, int t,
@@ -401,27 +431,28 @@ __global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y
   if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->k[cur ^ 1] = 0;
   u64 ahi = 0, alo = 0;
   const i64 stride = (i64)gridDim.x * blockDim.x;
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    double v[D];
+  const i64 npairs = (n + 1) >> 1;
+  for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
+    double2 in[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * n + i);
-    bool inside;
-    const u64 key = pack_key<D>(g, v, inside);
-    u32 s;
-    if (!inside || !tab.find(key, s)) {
-      atomicOr(&ctrl->error, kErrMissing);
-      continue;
-    }
-    double sq[D];
+    for (int j = 0; j < D; ++j) in[j] = __ldcs(reinterpret_cast<const double2*>(y + (i64)j * g.ld) + q);
+    double va[D], vb[D], oa[D], ob[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      const double nv = targets[(i64)s * D + j];
-      __stcs(yo + (i64)j * n + i, nv);
-      const double dlt = __dsub_rn(nv, v[j]);
-      sq[j] = __dmul_rn(dlt, dlt);
-    }
-    const u128 f = norm_to_fixed(__dsqrt_rn(row_sum<D>(sq)), g.movement_exp);
+    for (int j = 0; j < D; ++j) { va[j] = in[j].x; vb[j] = in[j].y; }
+    const double ma = shift_point<D>(g, tab, targets, va, oa, ctrl);
+    u128 f = norm_to_fixed(ma, g.movement_exp);
     add128(ahi, alo, (u64)(f >> 64), (u64)f);
+    if (2 * q + 1 < n) {
+      const double mb = shift_point<D>(g, tab, targets, vb, ob, ctrl);
+      f = norm_to_fixed(mb, g.movement_exp);
+      add128(ahi, alo, (u64)(f >> 64), (u64)f);
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) ob[j] = vb[j];
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      __stcs(reinterpret_cast<double2*>(yo + (i64)j * g.ld) + q, make_double2(oa[j], ob[j]));
   }
   // block reduction of the 128-bit movement
   for (int o = 16; o; o >>= 1) {
@@ -465,6 +496,140 @@ __global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y
     ctrl->iters = t + 1;
     ctrl->blocks_done = 0;
     if (mv < eta) ctrl->done = 1;
+  }
+}
+
+// ------------------------------------------------------------ spatial sort
+// One-time counting sort of the points by their initial cell (count-only
+// k_hist -> exclusive scan of the occupied cells' counts -> scatter).  All
+// later reductions are exact integer sums, so the order inside a cell is
+// irrelevant to the results; what the sort buys is that every warp sees
+// runs of equal cells -- and, from iteration 1 on, runs of identical
+// positions -- so the table atomics collapse to one per run.
+
+constexpr int kScanItems = 8;
+constexpr int kScanChunk = kThreads * kScanItems;
+
+template <int D>
+__device__ __forceinline__ u64 entry_count(const Entry<D>* ent, u32 s) { return ent[s].count; }
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_scan_reduce(const Entry<D>* ent, const u32* list, const u32* kp,
+                                                          u64* bsum) {
+  const u32 k = *kp;
+  const i64 a0 = (i64)blockIdx.x * kScanChunk;
+  u64 s = 0;
+  if (a0 < k) {
+    for (int it = 0; it < kScanItems; ++it) {
+      const i64 a = a0 + (i64)it * kThreads + threadIdx.x;
+      if (a < k) s += entry_count<D>(ent, list[a]);
+    }
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  __shared__ u64 w[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 t = 0;
+    for (int q = 0; q < kThreads / 32; ++q) t += w[q];
+    bsum[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of nb block sums, single block
+__global__ void __launch_bounds__(1024) k_scan_top(u64* bsum, int nb) {
+  __shared__ u64 w[32];
+  __shared__ u64 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const u64 v = i < nb ? bsum[i] : 0;
+    u64 x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 y = __shfl_up_sync(kFull, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) w[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      u64 z = w[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(kFull, z, o);
+        if (threadIdx.x >= o) z += y;
+      }
+      w[threadIdx.x] = z;
+    }
+    __syncthreads();
+    const u64 before = (threadIdx.x >= 32 ? w[(threadIdx.x >> 5) - 1] : 0) + x - v;
+    if (i < nb) bsum[i] = carry + before;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += before + v;
+    __syncthreads();
+  }
+}
+
+// per-cell write cursor = exclusive prefix of counts (list order)
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, const u32* list, const u32* kp,
+                                                         const u64* bsum, u32* off) {
+  const u32 k = *kp;
+  const i64 a0 = (i64)blockIdx.x * kScanChunk;
+  if (a0 >= k) return;
+  // thread t owns items a0 + t*kScanItems .. +kScanItems-1 (contiguous)
+  u64 c[kScanItems];
+  u64 tot = 0;
+  for (int it = 0; it < kScanItems; ++it) {
+    const i64 a = a0 + (i64)threadIdx.x * kScanItems + it;
+    c[it] = a < k ? entry_count<D>(ent, list[a]) : 0;
+    tot += c[it];
+  }
+  u64 x = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 y = __shfl_up_sync(kFull, x, o);
+    if ((threadIdx.x & 31) >= o) x += y;
+  }
+  __shared__ u64 w[kThreads / 32];
+  if ((threadIdx.x & 31) == 31) w[threadIdx.x >> 5] = x;
+  __syncthreads();
+  u64 pre = bsum[blockIdx.x] + x - tot;
+  for (int q = 0; q < (int)(threadIdx.x >> 5); ++q) pre += w[q];
+  for (int it = 0; it < kScanItems; ++it) {
+    const i64 a = a0 + (i64)threadIdx.x * kScanItems + it;
+    if (a < k) off[list[a]] = (u32)pre;
+    pre += c[it];
+  }
+}
+
+// scatter points into cell order; warp-aggregated cursor bumps
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__ y, double* __restrict__ ys, i64 n,
+                                                      GridParams g, Tab tab, u32* off, u32* perm, Ctrl* ctrl) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 base = warp * 32; base < n; base += nwarps * 32) {
+    const i64 i = base + lane;
+    double v[D];
+    u32 s = 0xffffffffu;
+    if (i < n) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * g.ld + i);
+      bool inside;
+      const u64 key = pack_key<D>(g, v, inside);
+      if (!inside || !tab.find(key, s)) { atomicOr(&ctrl->error, kErrMissing); s = 0xffffffffu; }
+    }
+    const unsigned peers = __match_any_sync(kFull, s);
+    const int leader = __ffs(peers) - 1;
+    u32 basepos = 0;
+    if (lane == leader && s != 0xffffffffu) basepos = atomicAdd(off + s, (u32)__popc(peers));
+    basepos = __shfl_sync(kFull, basepos, leader);
+    if (s != 0xffffffffu) {
+      const u32 pos = basepos + __popc(peers & ((1u << lane) - 1u));
+#pragma unroll
+      for (int j = 0; j < D; ++j) ys[(i64)j * g.ld + pos] = v[j];
+      perm[pos] = (u32)i;
+    }
   }
 }
 
@@ -567,7 +732,7 @@ __global__ void __launch_bounds__(kThreads) k_first(const double* __restrict__ y
     if (i < n) {
       double v[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = y[(i64)j * n + i];
+      for (int j = 0; j < D; ++j) v[j] = y[(i64)j * g.ld + i];
       bool inside;
       const u64 key = pack_key<D>(g, v, inside);
       u32 s;
@@ -630,7 +795,7 @@ __global__ void __launch_bounds__(kThreads) k_labels(const double* __restrict__ 
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     double v[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) v[j] = y[(i64)j * n + i];
+    for (int j = 0; j < D; ++j) v[j] = y[(i64)j * g.ld + i];
     bool inside;
     const u64 key = pack_key<D>(g, v, inside);
     u32 s = 0;

@@ -93,10 +93,12 @@ def _finish(ctx, labels, k, d, iters, mv, conv):
     return lab, tr
 
 
-def meanshiftpp(points: PointSet, cfg: ShiftConfig) -> tuple[Labeling, ShiftTrace]:
+def meanshiftpp(points: PointSet, cfg: ShiftConfig, labels_out: np.ndarray | None = None
+                ) -> tuple[Labeling, ShiftTrace]:
     """modeseek.py:125-146 on the B200: device-resident loop until the
     summed movement drops below eta (the converging step applied) or
-    max_iters, then device-side cluster extraction."""
+    max_iters, then device-side cluster extraction.  `labels_out` may be a
+    preallocated (n,) int64 array (e.g. pinned host memory)."""
     if not isinstance(points, PointSet):
         points = PointSet(points)
     L = _lib.load()
@@ -104,7 +106,9 @@ def meanshiftpp(points: PointSet, cfg: ShiftConfig) -> tuple[Labeling, ShiftTrac
     y = points.data
     n, d = y.shape
     eta = cfg.resolve_eta(n)
-    labels = np.empty(n, dtype=np.int64)
+    labels = np.empty(n, dtype=np.int64) if labels_out is None else labels_out
+    if labels.shape != (n,) or labels.dtype != np.int64 or not labels.flags.c_contiguous:
+        raise ValueError("labels_out must be a C-contiguous (n,) int64 array")
     mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
     k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
     _lib.check(L.gs_meanshiftpp(ctx, _lib.ptr(y), n, d, float(cfg.h), eta, int(cfg.max_iters),

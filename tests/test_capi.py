@@ -31,6 +31,21 @@ def test_header_declares_entry_points():
     assert names == sorted(_lib.SIGNATURES), "ctypes table must mirror the header"
 
 
+def declared_arity():
+    txt = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    out = {}
+    for m in re.finditer(r"GS_API\s+[\w\s\*]+?\b(gs_\w+)\s*\(([^)]*)\)", txt):
+        args = [a for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
+        out[m.group(1)] = len(args)
+    return out
+
+
+def test_ctypes_arity_matches_header():
+    ar = declared_arity()
+    for name, (_, args) in _lib.SIGNATURES.items():
+        assert len(args) == ar[name], name
+
+
 def test_library_exports_every_declared_symbol(lib):
     out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)],
                          capture_output=True, text=True, check=True).stdout
