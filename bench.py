@@ -216,10 +216,13 @@ def our_arm(a):
     cfg = gs.ShiftConfig(h=h, eta=eta, max_iters=mi)
     labels = torch.empty(x_dev.shape[0], dtype=torch.int64, device="cuda")
 
+    last = {}
+
     def step():
         if world > 1:
             return sharded.meanshiftpp_sharded(x_dev, cfg, labels, n_total=n)
         _, k, it, mv, conv = gs.meanshiftpp_device(x_dev, cfg, labels)
+        last["k"] = k
         return it
 
     def barrier():
@@ -243,6 +246,9 @@ def our_arm(a):
         torch.cuda.synchronize()
         barrier()
     ms = e0.elapsed_time(e1)
+    if world == 1:   # sanity (untimed): labels dense in [0, k)
+        u = torch.unique(labels)
+        assert int(u[0]) == 0 and int(u[-1]) == last["k"] - 1 and u.numel() == last["k"], "bad labels"
     prof = _lib.profile(2)
     _lib.profile(0)
     if world > 1:

@@ -648,6 +648,18 @@ __device__ __forceinline__ u32 uf_root(u32* par, u32 v) {
   return curr;
 }
 
+// Read-only root walk.  Used once all unions are done: a path-halving walk
+// here could overwrite another thread's freshly flattened par[s] = root
+// with an intermediate node.
+__device__ __forceinline__ u32 uf_root_ro(const u32* par, u32 v) {
+  u32 p = *(volatile const u32*)(par + v);
+  while (p != v) {
+    v = p;
+    p = *(volatile const u32*)(par + v);
+  }
+  return v;
+}
+
 __device__ __forceinline__ void uf_unite(u32* par, u32 a, u32 b) {
   u32 ra = uf_root(par, a), rb = uf_root(par, b);
   while (ra != rb) {
@@ -703,8 +715,8 @@ __global__ void k_uf_flatten(Tab tab, const u32* kp, u32* par, Entry<D>* acc) {
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
     const u32 s = tab.list[a];
-    const u32 r = uf_root(par, s);
-    par[s] = r;   // unions are complete: flattening is race-free
+    const u32 r = uf_root_ro(par, s);
+    par[s] = r;   // only the owner writes par[s]; every other write is a root
     const Entry<D>& e = tab.ent[s];
     Entry<D>* c = acc + r;
     atomicAdd(&c->count, e.count);
