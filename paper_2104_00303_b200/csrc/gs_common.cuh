@@ -45,7 +45,8 @@ struct GridParams {
   int qexp[GS_MAXD];       // s_j
   u64 nkeys;               // prod of extents
   u64 mask;                // hash mask (cap - 1) or 0 for dense tables
-  i64 ld;                  // SoA leading dimension of the iterate (n rounded up to 64)
+  i64 ld;                  // SoA leading dimension of the iterate (n rounded up to 128)
+  double inv_h;            // fl(1 / h), for cell_of_fast
 };
 
 // Device-resident loop control.  One per context.
@@ -132,8 +133,22 @@ __device__ __forceinline__ u128 norm_to_fixed(double m, int movement_exp) {
   return (((u128)hi) << 48) + (u128)lo;
 }
 
-// Floor of the IEEE quotient, as an integer-valued double.
+// Floor of the IEEE quotient fl(y / h), as an integer-valued double
+// (grid.py:81 `np.floor(data / h)`).
 __device__ __forceinline__ double cell_of(double y, double h) {
+  return floor(__ddiv_rn(y, h));
+}
+
+// Same value, cheaper: q = fl(y * fl(1/h)) is within |q| * 2^-51 of
+// Q = fl(y / h) (two roundings of 2^-53 each plus the reciprocal's), so
+// unless an integer lies within that distance of q, floor(q) == floor(Q).
+// Points near a cell face (and all non-finite cases) take the exact divide.
+__device__ __forceinline__ double cell_of_fast(double y, double h, double inv_h) {
+  const double q = __dmul_rn(y, inv_h);
+  const double f = floor(q);
+  const double r = __dsub_rn(q, f);   // exact: the fraction of a double
+  const double tol = fmax(fabs(q), 1.0) * 0x1p-50;
+  if (r > tol && r < 1.0 - tol) return f;
   return floor(__ddiv_rn(y, h));
 }
 

@@ -53,7 +53,7 @@ const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "shift", "clear
 
 constexpr int64_t kSortMinPoints = 1 << 15;   // spatial sort pays off above this
 
-inline int64_t soa_ld(int64_t n) { return (n + 63) & ~int64_t(63); }
+inline int64_t soa_ld(int64_t n) { return (n + 127) & ~int64_t(127); }   // = k_hist tile
 
 // Per-context kernel accounting: every launch is counted; with profiling on,
 // each launch is bracketed by CUDA events on the launching stream.
@@ -173,6 +173,7 @@ Plan make_plan(int64_t n, int d, double h, const InitStats& s) {
   memset(&g, 0, sizeof g);
   g.h = h;
   g.d = d;
+  g.inv_h = 1.0 / h;
   __int128 prod = 1;
   double span2 = 0.0;
   int64_t ext[GS_MAXD];
@@ -326,6 +327,28 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
                                                   static_cast<double*>(c->mv_hist.p), t, eta, cur); });
 }
 
+// Occupied-cell list of a table (hash tables maintain theirs on insert;
+// dense tables are compacted from their counts).  k must be 0 before.
+template <int D, class Tab>
+void build_list(gs_ctx* c, const Plan& p, Tab& tab) {
+  if constexpr (Tab::kDense) {
+    launch(c, K_CLEAR, [&] {
+      k_compact<D><<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(tab.ent, p.slots, tab.list, tab.k);
+    });
+  }
+}
+
+// Make a table clean whose list may not exist (dense tables in the loop).
+template <int D, class Tab>
+void clear_table(gs_ctx* c, const Plan& p, Tab& tab, u32* kp) {
+  if constexpr (Tab::kDense) {
+    launch(c, K_CLEAR, [&] { k_clear_all<D><<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(tab.ent, p.slots); });
+  } else {
+    launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<blocks_for(c, (int64_t)p.list_cap), kThreads, 0, c->st>>>(tab, kp); });
+  }
+  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(kp); });
+}
+
 // Extraction of y_final (modeseek.py:256-272).  Table buffer e is clean on
 // entry, buffer e^1 is dirty (cleared here and used as component scratch).
 template <int D, class Tab>
@@ -334,9 +357,9 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
-  launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e ^ 1], &ctrl->k[e ^ 1]); });
-  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e ^ 1]); });
+  clear_table<D>(c, p, tabs[e ^ 1], &ctrl->k[e ^ 1]);
   launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], ctrl, 0); });
+  build_list<D>(c, p, tabs[e]);
   u32* par = ensure<u32>(c, c->par, p.slots);
   u32* first = ensure<u32>(c, c->first, p.slots);
   u32* rankmap = ensure<u32>(c, c->aux, p.slots);
@@ -398,6 +421,7 @@ const u32* spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   double* y0 = static_cast<double*>(c->y[0].p);
   double* y1 = static_cast<double*>(c->y[1].p);
   launch(c, K_SORT, [&] { k_hist<D, Tab, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
+  build_list<D>(c, p, tabs[0]);
   launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, tabs[0].list, &ctrl->k[0], bsum); });
   launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
   launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, tabs[0].list, &ctrl->k[0], bsum, off); });
@@ -432,6 +456,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   u64* fp = ensure<u64>(c, c->fp_hist, (size_t)max_iters);
   ensure<u32>(c, c->k_hist, (size_t)max_iters);
   GS_CUDA(cudaMemsetAsync(fp, 0, sizeof(u64) * max_iters, c->st));
+  GS_CUDA(cudaMemsetAsync(c->k_hist.p, 0, sizeof(u32) * max_iters, c->st));
   reset_ctrl(c);
   const u32* perm = nullptr;
   if (n >= kSortMinPoints)
@@ -508,18 +533,17 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
   ensure<double>(c, c->mv_hist, 1);
-  ensure<u64>(c, c->fp_hist, 1);
-  ensure<u32>(c, c->k_hist, 1);
+  GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->fp_hist, 1), 0, 8, c->st));
+  GS_CUDA(cudaMemsetAsync(ensure<u32>(c, c->k_hist, 1), 0, 4, c->st));
   reset_ctrl(c);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   if (p.dense) {
     enqueue_iteration<D>(c, p, tabs.dn, 0, -1.0, n, nb_pts, nb_cells);
-    launch(c, K_CLEAR, [&] { k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.dn[0], &ctrl->k[0]); });
+    clear_table<D>(c, p, tabs.dn[0], &ctrl->k[0]);
   } else {
     enqueue_iteration<D>(c, p, tabs.hs, 0, -1.0, n, nb_pts, nb_cells);
-    launch(c, K_CLEAR, [&] { k_clear<D><<<nb_cells, kThreads, 0, c->st>>>(tabs.hs[0], &ctrl->k[0]); });
+    clear_table<D>(c, p, tabs.hs[0], &ctrl->k[0]);
   }
-  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]); });
   double* aos = ensure<double>(c, c->x_stage, (size_t)n * D);
   launch(c, K_XPOSE, [&] { k_soa_to_aos<D><<<nb_pts, kThreads, 0, c->st>>>(y1, aos, n, p.g.ld); });
   check_launch();
@@ -596,6 +620,7 @@ int64_t run_tables_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t
   const int nb_pts = blocks_for(c, n);
   if (p.dense) {
     launch(c, K_HIST, [&] { k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.dn[0], ctrl, 0); });
+    build_list<D>(c, p, tabs.dn[0]);
     return dump_tables<D>(c, p, tabs.dn, cap, cells, counts, sums, nc, ns);
   }
   launch(c, K_HIST, [&] { k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.hs[0], ctrl, 0); });

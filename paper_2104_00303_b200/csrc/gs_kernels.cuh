@@ -124,7 +124,7 @@ __device__ __forceinline__ u64 pack_key(const GridParams& g, const double* v, bo
   inside = true;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    const i64 c = (i64)cell_of(v[j], g.h);
+    const i64 c = (i64)cell_of_fast(v[j], g.h, g.inv_h);
     inside &= (c >= g.lo[j]) & (c <= g.hi[j]);
     key += (u64)(c - g.base[j]) * g.stride[j];
   }
@@ -252,83 +252,166 @@ __global__ void k_soa_to_aos(const double* __restrict__ y, double* __restrict__ 
 
 // --------------------------------------------------------------- k_hist
 
+// Partial aggregate of a run of points: count and split fixed-point sums.
+template <int D>
+struct Agg {
+  u32 cnt;
+  i64 hi[D];
+  u64 lo[D];
+  __device__ __forceinline__ void zero() {
+    cnt = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { hi[j] = 0; lo[j] = 0; }
+  }
+  __device__ __forceinline__ void add(const Agg& o) {
+    cnt += o.cnt;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { hi[j] += o.hi[j]; lo[j] += o.lo[j]; }
+  }
+  __device__ __forceinline__ Agg shfl_up(int off) const {
+    Agg r;
+    r.cnt = __shfl_up_sync(kFull, cnt, off);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      r.hi[j] = (i64)__shfl_up_sync(kFull, (unsigned long long)hi[j], off);
+      r.lo[j] = __shfl_up_sync(kFull, lo[j], off);
+    }
+    return r;
+  }
+};
+
+// Flush one finished segment (a run of points with the same cell key).
+template <int D, class Tab, bool CountOnly>
+__device__ __forceinline__ void flush_segment(const Tab& tab, Ctrl* ctrl, u64 key, const Agg<D>& a) {
+  if (key == kEmpty || a.cnt == 0) return;
+  bool fresh;
+  const u32 s = tab.insert(key, fresh, &ctrl->error);
+  if (s == 0xffffffffu) return;
+  Entry<D>* e = tab.ent + s;
+  // dense tables: no-return atomics (RED); occupancy is read back from the
+  // counts where a cell list is needed (k_compact)
+  atomicAdd(&e->count, (u64)a.cnt);
+  if constexpr (!Tab::kDense) {
+    if (fresh) tab.list[atomicAdd(tab.k, 1u)] = s;
+  }
+  if constexpr (!CountOnly) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      atomicAdd(&e->hi[j], (u64)a.hi[j]);
+      atomicAdd(&e->lo[j], a.lo[j]);
+    }
+  }
+}
+
+// Warp reduce-by-key over a 128-point tile (4 consecutive points per lane):
+// in-lane sequential aggregation, one segmented inclusive scan of the lane
+// tail aggregates across the warp, then every segment is flushed once, by
+// the lane holding its successor's head (lane 31 flushes the tile's last
+// segment).  Once the points are cell-sorted a tile holds one or two
+// segments, so the table sees ~7-14 atomics per 128 points.
 template <int D, class Tab, bool CountOnly = false>
 __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y, i64 n, GridParams g,
                                                    Tab tab, Ctrl* ctrl, int check_done) {
   if (check_done && *(volatile int*)&ctrl->done) return;
+  constexpr int P = 4;
   const int lane = threadIdx.x & 31;
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  for (i64 base = warp * 32; base < n; base += nwarps * 32) {
-    const i64 i = base + lane;
-    u64 key = kEmpty;
-    i64 fx[D];
+  for (i64 base = warp * 32 * P; base < n; base += nwarps * 32 * P) {
+    const i64 i0 = base + P * lane;
+    double v[P][D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) fx[j] = 0;
-    if (i < n) {
-      double v[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * g.ld + i);
-      bool inside;
-      key = pack_key<D>(g, v, inside);
-      if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
-      if constexpr (!CountOnly) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) fx[j] = to_fixed(v[j], g.qscale[j]);
-      }
+    for (int j = 0; j < D; ++j) {
+      const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld + i0);
+      const double2 a = __ldcs(src), b = __ldcs(src + 1);
+      v[0][j] = a.x; v[1][j] = a.y; v[2][j] = b.x; v[3][j] = b.y;
     }
-    // segments: maximal runs of consecutive lanes with the same key
-    const u64 pkey = __shfl_up_sync(kFull, key, 1);
-    const bool same_prev = (lane > 0) && (pkey == key);
-    bool same_val = true;
+    u64 key[P];
+    Agg<D> it[P];
 #pragma unroll
-    for (int j = 0; j < D; ++j) same_val &= ((i64)__shfl_up_sync(kFull, (unsigned long long)fx[j], 1) == fx[j]);
-    const u32 heads = __ballot_sync(kFull, !same_prev);
-    const u32 mixed = CountOnly ? 0u : __ballot_sync(kFull, same_prev && !same_val);
-    const u32 after = (lane == 31) ? 0u : (heads & (~0u << (lane + 1)));
-    const int end = after ? (__ffs(after) - 1) : 32;
-    i64 shi[D];
-    u64 slo[D];
-    if (mixed == 0) {
-      // every segment carries one value: head contributes count * value
-      const i64 cnt = end - lane;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        shi[j] = (fx[j] >> 32) * cnt;
-        slo[j] = (u64)(fx[j] & 0xffffffffll) * (u64)cnt;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        shi[j] = fx[j] >> 32;
-        slo[j] = (u64)(fx[j] & 0xffffffffll);
-      }
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const i64 oh = (i64)__shfl_down_sync(kFull, (unsigned long long)shi[j], off);
-          const u64 ol = __shfl_down_sync(kFull, slo[j], off);
-          if (lane + off < end) { shi[j] += oh; slo[j] += ol; }
-        }
-      }
-    }
-    if (!same_prev && key != kEmpty) {
-      const u64 cnt = (u64)(end - lane);
-      bool fresh;
-      const u32 s = tab.insert(key, fresh, &ctrl->error);
-      if (s != 0xffffffffu) {
-        Entry<D>* e = tab.ent + s;
-        const u64 old = atomicAdd(&e->count, cnt);
-        if (Tab::kDense ? (old == 0) : fresh) tab.list[atomicAdd(tab.k, 1u)] = s;
+    for (int m = 0; m < P; ++m) {
+      key[m] = kEmpty;
+      it[m].zero();
+      if (i0 + m < n) {
+        bool inside;
+        key[m] = pack_key<D>(g, v[m], inside);
+        if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+        it[m].cnt = 1;
         if constexpr (!CountOnly) {
 #pragma unroll
           for (int j = 0; j < D; ++j) {
-            atomicAdd(&e->hi[j], (u64)shi[j]);
-            atomicAdd(&e->lo[j], slo[j]);
+            const i64 f = to_fixed(v[m][j], g.qscale[j]);
+            it[m].hi[j] = f >> 32;
+            it[m].lo[j] = (u64)(f & 0xffffffffll);
           }
         }
       }
+    }
+    const u64 prevkey = __shfl_up_sync(kFull, key[P - 1], 1);
+    bool head[P];
+    head[0] = (lane == 0) || (key[0] != prevkey);
+#pragma unroll
+    for (int m = 1; m < P; ++m) head[m] = key[m] != key[m - 1];
+    // tail aggregate of this lane (items from its last head on)
+    Agg<D> tail;
+    tail.zero();
+    bool hashead = false;
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+      if (head[m]) { tail.zero(); hashead = true; }
+      tail.add(it[m]);
+    }
+    // segmented inclusive scan over lanes: x_L = tail_L + (hashead_L ? 0 : x_{L-1})
+    Agg<D> x = tail;
+    bool f = hashead;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const Agg<D> yv = x.shfl_up(off);
+      const bool yf = __shfl_up_sync(kFull, f, off);
+      if (lane >= off && !f) { x.add(yv); f = yf; }
+    }
+    Agg<D> acc = x.shfl_up(1);   // open segment carried in from the lanes before
+    if (lane == 0) acc.zero();
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+      if (head[m]) {
+        if (m > 0 || lane > 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, m ? key[m - 1] : prevkey, acc);
+        acc = it[m];
+      } else {
+        acc.add(it[m]);
+      }
+    }
+    if (lane == 31) flush_segment<D, Tab, CountOnly>(tab, ctrl, key[P - 1], acc);
+  }
+}
+
+// Dense tables: occupied-cell list from the counts (warp-aggregated append).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_compact(const Entry<D>* ent, u64 nslots, u32* list, u32* kp) {
+  const int lane = threadIdx.x & 31;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 t0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  for (i64 base = t0 - lane; base < (i64)nslots; base += stride) {
+    const i64 s = base + lane;
+    const bool occ = s < (i64)nslots && ent[s].count != 0;
+    const u32 m = __ballot_sync(kFull, occ);
+    u32 at = 0;
+    if (lane == 0 && m) at = atomicAdd(kp, (u32)__popc(m));
+    at = __shfl_sync(kFull, at, 0);
+    if (occ) list[at + __popc(m & ((1u << lane) - 1u))] = (u32)s;
+  }
+}
+
+// Dense tables: zero every occupied slot (no list needed).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_clear_all(Entry<D>* ent, u64 nslots) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < (i64)nslots; s += stride) {
+    Entry<D>* e = ent + s;
+    if (e->count) {
+      e->count = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) { e->hi[j] = 0; e->lo[j] = 0; }
     }
   }
 }
@@ -362,37 +445,69 @@ __device__ __forceinline__ void neighbourhood_sum(const GridParams& g, const Tab
 }
 
 template <int D, class Tab>
+__device__ __forceinline__ void agg_cell(const GridParams& g, const Tab& tab, u32 s, double* __restrict__ targets,
+                                         u64& fp) {
+  const u64 key = tab.key_of(s);
+  u64 cnt;
+  i128 sum[D];
+  neighbourhood_sum<D>(g, tab, key, cnt, sum);
+  const double c = (double)cnt;
+#pragma unroll
+  for (int j = 0; j < D; ++j) targets[(i64)s * D + j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
+  fp += cell_fingerprint<D>(g, key, tab.ent[s].count);
+}
+
+// Per occupied cell: 3^d neighbourhood -> target mean.  Dense tables are
+// walked slot by slot (empty slots are one 8-byte read); hash tables by
+// their occupied list.  Also clears the previous iteration's table and
+// records k and the (cells, counts) fingerprint of this iteration.
+template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab prev, double* __restrict__ targets,
                                                   Ctrl* ctrl, int cur, u64* fp_out, u32* k_out) {
   if (*(volatile int*)&ctrl->done) return;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  // clear the previous iteration's table (no longer referenced)
-  const u32 kp = ctrl->k[cur ^ 1];
-  for (i64 a = tid; a < kp; a += stride) {
-    const u32 s = prev.list[a];
-    Entry<D>* e = prev.ent + s;
-    e->count = 0;
-#pragma unroll
-    for (int j = 0; j < D; ++j) { e->hi[j] = 0; e->lo[j] = 0; }
-    if constexpr (!Tab::kDense) prev.keys[s] = kEmpty;
-  }
-  const u32 k = ctrl->k[cur];
   u64 fp = 0;
-  for (i64 a = tid; a < k; a += stride) {
-    const u32 s = tab.list[a];
-    const u64 key = tab.key_of(s);
-    u64 cnt;
-    i128 sum[D];
-    neighbourhood_sum<D>(g, tab, key, cnt, sum);
-    const double c = (double)cnt;
+  u32 kc = 0;
+  if constexpr (Tab::kDense) {
+    const i64 ns = (i64)g.nkeys;
+    for (i64 s = tid; s < ns; s += stride) {
+      Entry<D>* e = prev.ent + s;
+      if (e->count) {
+        e->count = 0;
 #pragma unroll
-    for (int j = 0; j < D; ++j) targets[(i64)s * D + j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
-    fp += cell_fingerprint<D>(g, key, tab.ent[s].count);
+        for (int j = 0; j < D; ++j) { e->hi[j] = 0; e->lo[j] = 0; }
+      }
+    }
+    for (i64 s = tid; s < ns; s += stride) {
+      if (tab.ent[s].count == 0) continue;
+      agg_cell<D>(g, tab, (u32)s, targets, fp);
+      ++kc;
+    }
+  } else {
+    const u32 kp = ctrl->k[cur ^ 1];
+    for (i64 a = tid; a < kp; a += stride) {
+      const u32 s = prev.list[a];
+      Entry<D>* e = prev.ent + s;
+      e->count = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) { e->hi[j] = 0; e->lo[j] = 0; }
+      prev.keys[s] = kEmpty;
+    }
+    const u32 k = ctrl->k[cur];
+    for (i64 a = tid; a < k; a += stride) {
+      agg_cell<D>(g, tab, tab.list[a], targets, fp);
+      ++kc;
+    }
   }
-  for (int o = 16; o; o >>= 1) fp += __shfl_xor_sync(kFull, fp, o);
-  if ((threadIdx.x & 31) == 0 && fp) atomicAdd((unsigned long long*)fp_out, (unsigned long long)fp);
-  if (tid == 0 && k_out) *k_out = k;
+  for (int o = 16; o; o >>= 1) {
+    fp += __shfl_xor_sync(kFull, fp, o);
+    kc += __shfl_xor_sync(kFull, kc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (fp) atomicAdd((unsigned long long*)fp_out, (unsigned long long)fp);
+    if (kc) atomicAdd(k_out, kc);
+  }
 }
 
 // -------------------------------------------------------------- k_shift
@@ -420,8 +535,8 @@ __device__ __forceinline__ double shift_point(const GridParams& g, const Tab& ta
   return __dsqrt_rn(row_sum<D>(sq));
 }
 
-// Two consecutive points per thread and loop trip (16-byte vector loads of
-// each SoA axis); streaming loads/stores keep the cell tables in L2.
+// Four consecutive points per thread and loop trip (two 16-byte vector
+// loads per SoA axis); streaming loads/stores keep the cell tables in L2.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
                                                     GridParams g, Tab tab, const double* __restrict__ targets,
@@ -431,28 +546,36 @@ __global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y
   if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->k[cur ^ 1] = 0;
   u64 ahi = 0, alo = 0;
   const i64 stride = (i64)gridDim.x * blockDim.x;
-  const i64 npairs = (n + 1) >> 1;
-  for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
-    double2 in[D];
+  const i64 nquads = (n + 3) >> 2;
+  for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < nquads; q += stride) {
+    double2 in[D][2];
 #pragma unroll
-    for (int j = 0; j < D; ++j) in[j] = __ldcs(reinterpret_cast<const double2*>(y + (i64)j * g.ld) + q);
-    double va[D], vb[D], oa[D], ob[D];
+    for (int j = 0; j < D; ++j) {
+      const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld) + 2 * q;
+      in[j][0] = __ldcs(src);
+      in[j][1] = __ldcs(src + 1);
+    }
+    double out[4][D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) { va[j] = in[j].x; vb[j] = in[j].y; }
-    const double ma = shift_point<D>(g, tab, targets, va, oa, ctrl);
-    u128 f = norm_to_fixed(ma, g.movement_exp);
-    add128(ahi, alo, (u64)(f >> 64), (u64)f);
-    if (2 * q + 1 < n) {
-      const double mb = shift_point<D>(g, tab, targets, vb, ob, ctrl);
-      f = norm_to_fixed(mb, g.movement_exp);
-      add128(ahi, alo, (u64)(f >> 64), (u64)f);
-    } else {
+    for (int m = 0; m < 4; ++m) {
+      double v[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) ob[j] = vb[j];
+      for (int j = 0; j < D; ++j) v[j] = (m & 1) ? in[j][m >> 1].y : in[j][m >> 1].x;
+      if (4 * q + m < n) {
+        const double mv = shift_point<D>(g, tab, targets, v, out[m], ctrl);
+        const u128 f = norm_to_fixed(mv, g.movement_exp);
+        add128(ahi, alo, (u64)(f >> 64), (u64)f);
+      } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[m][j] = v[j];
+      }
     }
 #pragma unroll
-    for (int j = 0; j < D; ++j)
-      __stcs(reinterpret_cast<double2*>(yo + (i64)j * g.ld) + q, make_double2(oa[j], ob[j]));
+    for (int j = 0; j < D; ++j) {
+      double2* dst = reinterpret_cast<double2*>(yo + (i64)j * g.ld) + 2 * q;
+      __stcs(dst, make_double2(out[0][j], out[1][j]));
+      __stcs(dst + 1, make_double2(out[2][j], out[3][j]));
+    }
   }
   // block reduction of the 128-bit movement
   for (int o = 16; o; o >>= 1) {
