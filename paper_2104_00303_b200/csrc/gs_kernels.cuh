@@ -326,23 +326,75 @@ __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y,
       const double2 a = __ldcs(src), b = __ldcs(src + 1);
       v[0][j] = a.x; v[1][j] = a.y; v[2][j] = b.x; v[3][j] = b.y;
     }
+    // identical consecutive points (every cell-sorted run after iteration
+    // 0) are binned and quantised once: exact, and 4x less arithmetic
+    bool uni = i0 + P - 1 < n;
+#pragma unroll
+    for (int m = 1; m < P; ++m)
+#pragma unroll
+      for (int j = 0; j < D; ++j) uni &= __double_as_longlong(v[m][j]) == __double_as_longlong(v[0][j]);
+    // whole tile one value: a single flush, no warp scan
+    bool same = uni;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      same &= __shfl_sync(kFull, __double_as_longlong(v[0][j]), 0) == __double_as_longlong(v[0][j]);
+    if (__all_sync(kFull, same)) {
+      if (lane == 0) {
+        bool inside;
+        const u64 k0 = pack_key<D>(g, v[0], inside);
+        if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+        Agg<D> t;
+        t.zero();
+        t.cnt = 32 * P;
+        if constexpr (!CountOnly) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const i64 f = to_fixed(v[0][j], g.qscale[j]);
+            t.hi[j] = (f >> 32) * (32 * P);
+            t.lo[j] = (u64)(f & 0xffffffffll) * (32 * P);
+          }
+        }
+        flush_segment<D, Tab, CountOnly>(tab, ctrl, k0, t);
+      }
+      continue;
+    }
     u64 key[P];
     Agg<D> it[P];
 #pragma unroll
     for (int m = 0; m < P; ++m) {
       key[m] = kEmpty;
       it[m].zero();
-      if (i0 + m < n) {
-        bool inside;
-        key[m] = pack_key<D>(g, v[m], inside);
-        if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
-        it[m].cnt = 1;
-        if constexpr (!CountOnly) {
+    }
+    if (uni) {
+      bool inside;
+      const u64 k0 = pack_key<D>(g, v[0], inside);
+      if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
 #pragma unroll
-          for (int j = 0; j < D; ++j) {
-            const i64 f = to_fixed(v[m][j], g.qscale[j]);
-            it[m].hi[j] = f >> 32;
-            it[m].lo[j] = (u64)(f & 0xffffffffll);
+      for (int m = 0; m < P; ++m) key[m] = k0;
+      it[0].cnt = P;
+      if constexpr (!CountOnly) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const i64 f = to_fixed(v[0][j], g.qscale[j]);
+          it[0].hi[j] = (f >> 32) * P;
+          it[0].lo[j] = (u64)(f & 0xffffffffll) * P;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        if (i0 + m < n) {
+          bool inside;
+          key[m] = pack_key<D>(g, v[m], inside);
+          if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+          it[m].cnt = 1;
+          if constexpr (!CountOnly) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              const i64 f = to_fixed(v[m][j], g.qscale[j]);
+              it[m].hi[j] = f >> 32;
+              it[m].lo[j] = (u64)(f & 0xffffffffll);
+            }
           }
         }
       }
@@ -556,18 +608,36 @@ __global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y
       in[j][1] = __ldcs(src + 1);
     }
     double out[4][D];
+    bool uni = 4 * q + 3 < n;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
+    for (int j = 0; j < D; ++j)
+      uni &= (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][0].y)) &
+             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].x)) &
+             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].y));
+    if (uni) {
+      // four identical points: one lookup, one norm, movement x4 (exact)
       double v[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = (m & 1) ? in[j][m >> 1].y : in[j][m >> 1].x;
-      if (4 * q + m < n) {
-        const double mv = shift_point<D>(g, tab, targets, v, out[m], ctrl);
-        const u128 f = norm_to_fixed(mv, g.movement_exp);
-        add128(ahi, alo, (u64)(f >> 64), (u64)f);
-      } else {
+      for (int j = 0; j < D; ++j) v[j] = in[j][0].x;
+      const double mv = shift_point<D>(g, tab, targets, v, out[0], ctrl);
+      const u128 f = norm_to_fixed(mv, g.movement_exp) << 2;
+      add128(ahi, alo, (u64)(f >> 64), (u64)f);
 #pragma unroll
-        for (int j = 0; j < D; ++j) out[m][j] = v[j];
+      for (int j = 0; j < D; ++j) out[1][j] = out[2][j] = out[3][j] = out[0][j];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        double v[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) v[j] = (m & 1) ? in[j][m >> 1].y : in[j][m >> 1].x;
+        if (4 * q + m < n) {
+          const double mv = shift_point<D>(g, tab, targets, v, out[m], ctrl);
+          const u128 f = norm_to_fixed(mv, g.movement_exp);
+          add128(ahi, alo, (u64)(f >> 64), (u64)f);
+        } else {
+#pragma unroll
+          for (int j = 0; j < D; ++j) out[m][j] = v[j];
+        }
       }
     }
 #pragma unroll
