@@ -413,21 +413,22 @@ template <int D, class Tab>
 const u32* spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
-  const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
-  const int nbs = (int)((p.list_cap + kScanChunk - 1) / kScanChunk);
+  // dense: scan every slot in key order (lexicographic cell order);
+  // hash: scan the occupied list (first-touch order)
+  const u64 nitems = Tab::kDense ? p.slots : p.list_cap;
+  const int nbs = (int)((nitems + kScanChunk - 1) / kScanChunk);
   u64* bsum = ensure<u64>(c, c->scan, (size_t)nbs + 1);
   u32* off = ensure<u32>(c, c->aux, p.slots);
   u32* perm = ensure<u32>(c, c->perm, (size_t)n);
   double* y0 = static_cast<double*>(c->y[0].p);
   double* y1 = static_cast<double*>(c->y[1].p);
+  const u32* list = Tab::kDense ? nullptr : tabs[0].list;
   launch(c, K_SORT, [&] { k_hist<D, Tab, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
-  build_list<D>(c, p, tabs[0]);
-  launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, tabs[0].list, &ctrl->k[0], bsum); });
+  launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, p.slots); });
   launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
-  launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, tabs[0].list, &ctrl->k[0], bsum, off); });
+  launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, off, p.slots); });
   launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, y1, n, p.g, tabs[0], off, perm, ctrl); });
-  launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[0], &ctrl->k[0]); });
-  launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[0]); });
+  clear_table<D>(c, p, tabs[0], &ctrl->k[0]);
   check_launch();
   std::swap(c->y[0], c->y[1]);
   return perm;

@@ -303,22 +303,31 @@ __device__ __forceinline__ void flush_segment(const Tab& tab, Ctrl* ctrl, u64 ke
   }
 }
 
-// Warp reduce-by-key over a 128-point tile (4 consecutive points per lane):
-// in-lane sequential aggregation, one segmented inclusive scan of the lane
-// tail aggregates across the warp, then every segment is flushed once, by
-// the lane holding its successor's head (lane 31 flushes the tile's last
-// segment).  Once the points are cell-sorted a tile holds one or two
-// segments, so the table sees ~7-14 atomics per 128 points.
+// Warp reduce-by-key: each warp owns a contiguous chunk of 128-point tiles
+// (4 consecutive points per lane).  Per tile: in-lane sequential
+// aggregation, one segmented inclusive scan of the lane tail aggregates,
+// and every finished segment is flushed once by the lane holding its
+// successor's head.  The open segment at the end of a tile is carried into
+// the next tile (not flushed), so a run of one cell spanning the whole chunk
+// costs one flush: hot cells (a mode can hold ~2% of all points) would
+// otherwise serialise thousands of atomics on one L2 line per iteration.
 template <int D, class Tab, bool CountOnly = false>
 __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y, i64 n, GridParams g,
                                                    Tab tab, Ctrl* ctrl, int check_done) {
   if (check_done && *(volatile int*)&ctrl->done) return;
   constexpr int P = 4;
+  constexpr int TILE = 32 * P;
   const int lane = threadIdx.x & 31;
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  for (i64 base = warp * 32 * P; base < n; base += nwarps * 32 * P) {
-    const i64 i0 = base + P * lane;
+  const i64 ntiles = (n + TILE - 1) / TILE;
+  const i64 per = (ntiles + nwarps - 1) / nwarps;
+  const i64 t_end = min(ntiles, (warp + 1) * per);
+  u64 ckey = kEmpty;          // carried open segment (uniform across lanes)
+  Agg<D> cagg;
+  cagg.zero();
+  for (i64 tile = warp * per; tile < t_end; ++tile) {
+    const i64 i0 = tile * TILE + P * lane;
     double v[P][D];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
@@ -333,28 +342,32 @@ __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y,
     for (int m = 1; m < P; ++m)
 #pragma unroll
       for (int j = 0; j < D; ++j) uni &= __double_as_longlong(v[m][j]) == __double_as_longlong(v[0][j]);
-    // whole tile one value: a single flush, no warp scan
     bool same = uni;
 #pragma unroll
     for (int j = 0; j < D; ++j)
       same &= __shfl_sync(kFull, __double_as_longlong(v[0][j]), 0) == __double_as_longlong(v[0][j]);
     if (__all_sync(kFull, same)) {
-      if (lane == 0) {
-        bool inside;
-        const u64 k0 = pack_key<D>(g, v[0], inside);
-        if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
-        Agg<D> t;
-        t.zero();
-        t.cnt = 32 * P;
-        if constexpr (!CountOnly) {
+      // whole tile one value (all lanes hold it): merge into the carry
+      bool inside;
+      const u64 k0 = pack_key<D>(g, v[0], inside);
+      if (!inside && lane == 0) atomicOr(&ctrl->error, kErrOutOfBox);
+      Agg<D> t;
+      t.zero();
+      t.cnt = TILE;
+      if constexpr (!CountOnly) {
 #pragma unroll
-          for (int j = 0; j < D; ++j) {
-            const i64 f = to_fixed(v[0][j], g.qscale[j]);
-            t.hi[j] = (f >> 32) * (32 * P);
-            t.lo[j] = (u64)(f & 0xffffffffll) * (32 * P);
-          }
+        for (int j = 0; j < D; ++j) {
+          const i64 f = to_fixed(v[0][j], g.qscale[j]);
+          t.hi[j] = (f >> 32) * TILE;
+          t.lo[j] = (u64)(f & 0xffffffffll) * TILE;
         }
-        flush_segment<D, Tab, CountOnly>(tab, ctrl, k0, t);
+      }
+      if (k0 == ckey) {
+        cagg.add(t);
+      } else {
+        if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
+        ckey = k0;
+        cagg = t;
       }
       continue;
     }
@@ -399,14 +412,16 @@ __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y,
         }
       }
     }
-    const u64 prevkey = __shfl_up_sync(kFull, key[P - 1], 1);
+    u64 prevkey = __shfl_up_sync(kFull, key[P - 1], 1);
+    if (lane == 0) prevkey = ckey;
     bool head[P];
-    head[0] = (lane == 0) || (key[0] != prevkey);
+    head[0] = key[0] != prevkey;
 #pragma unroll
     for (int m = 1; m < P; ++m) head[m] = key[m] != key[m - 1];
-    // tail aggregate of this lane (items from its last head on)
+    // tail aggregate of this lane (items from its last head on); lane 0
+    // starts from the carry when its first item continues it
     Agg<D> tail;
-    tail.zero();
+    if (lane == 0 && !head[0]) tail = cagg; else tail.zero();
     bool hashead = false;
 #pragma unroll
     for (int m = 0; m < P; ++m) {
@@ -423,18 +438,26 @@ __global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y,
       if (lane >= off && !f) { x.add(yv); f = yf; }
     }
     Agg<D> acc = x.shfl_up(1);   // open segment carried in from the lanes before
-    if (lane == 0) acc.zero();
+    if (lane == 0) acc = cagg;
 #pragma unroll
     for (int m = 0; m < P; ++m) {
       if (head[m]) {
-        if (m > 0 || lane > 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, m ? key[m - 1] : prevkey, acc);
+        flush_segment<D, Tab, CountOnly>(tab, ctrl, m ? key[m - 1] : prevkey, acc);
         acc = it[m];
       } else {
         acc.add(it[m]);
       }
     }
-    if (lane == 31) flush_segment<D, Tab, CountOnly>(tab, ctrl, key[P - 1], acc);
+    // lane 31's open segment becomes the carry
+    ckey = __shfl_sync(kFull, key[P - 1], 31);
+    cagg.cnt = __shfl_sync(kFull, acc.cnt, 31);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      cagg.hi[j] = (i64)__shfl_sync(kFull, (unsigned long long)acc.hi[j], 31);
+      cagg.lo[j] = __shfl_sync(kFull, acc.lo[j], 31);
+    }
   }
+  if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
 }
 
 // Dense tables: occupied-cell list from the counts (warp-aggregated append).
@@ -590,7 +613,7 @@ __device__ __forceinline__ double shift_point(const GridParams& g, const Tab& ta
 // Four consecutive points per thread and loop trip (two 16-byte vector
 // loads per SoA axis); streaming loads/stores keep the cell tables in L2.
 template <int D, class Tab>
-__global__ void __launch_bounds__(kThreads) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
+__global__ void __launch_bounds__(kThreads, 3) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
                                                     GridParams g, Tab tab, const double* __restrict__ targets,
                                                     Ctrl* ctrl, u64* partials, double* mv_hist, int t,
                                                     double eta, int cur) {
@@ -706,16 +729,21 @@ constexpr int kScanChunk = kThreads * kScanItems;
 template <int D>
 __device__ __forceinline__ u64 entry_count(const Entry<D>* ent, u32 s) { return ent[s].count; }
 
+// Items are either the entries of an occupied list (list != nullptr, count
+// *kp) or, for dense tables, every slot in key order (count nslots) -- the
+// latter makes the sorted point order the lexicographic cell order.
+__device__ __forceinline__ u32 scan_item(const u32* list, i64 a) { return list ? list[a] : (u32)a; }
+
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_scan_reduce(const Entry<D>* ent, const u32* list, const u32* kp,
-                                                          u64* bsum) {
-  const u32 k = *kp;
+                                                          u64* bsum, u64 nslots) {
+  const u64 k = list ? (u64)*kp : nslots;
   const i64 a0 = (i64)blockIdx.x * kScanChunk;
   u64 s = 0;
   if (a0 < k) {
     for (int it = 0; it < kScanItems; ++it) {
       const i64 a = a0 + (i64)it * kThreads + threadIdx.x;
-      if (a < k) s += entry_count<D>(ent, list[a]);
+      if (a < (i64)k) s += entry_count<D>(ent, scan_item(list, a));
     }
   }
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
@@ -765,16 +793,16 @@ __global__ void __launch_bounds__(1024) k_scan_top(u64* bsum, int nb) {
 // per-cell write cursor = exclusive prefix of counts (list order)
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, const u32* list, const u32* kp,
-                                                         const u64* bsum, u32* off) {
-  const u32 k = *kp;
+                                                         const u64* bsum, u32* off, u64 nslots) {
+  const u64 k = list ? (u64)*kp : nslots;
   const i64 a0 = (i64)blockIdx.x * kScanChunk;
-  if (a0 >= k) return;
+  if (a0 >= (i64)k) return;
   // thread t owns items a0 + t*kScanItems .. +kScanItems-1 (contiguous)
   u64 c[kScanItems];
   u64 tot = 0;
   for (int it = 0; it < kScanItems; ++it) {
     const i64 a = a0 + (i64)threadIdx.x * kScanItems + it;
-    c[it] = a < k ? entry_count<D>(ent, list[a]) : 0;
+    c[it] = a < (i64)k ? entry_count<D>(ent, scan_item(list, a)) : 0;
     tot += c[it];
   }
   u64 x = tot;
@@ -789,7 +817,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, co
   for (int q = 0; q < (int)(threadIdx.x >> 5); ++q) pre += w[q];
   for (int it = 0; it < kScanItems; ++it) {
     const i64 a = a0 + (i64)threadIdx.x * kScanItems + it;
-    if (a < k) off[list[a]] = (u32)pre;
+    if (a < (i64)k) off[scan_item(list, a)] = (u32)pre;
     pre += c[it];
   }
 }
