@@ -136,6 +136,23 @@ def test_run_vs_reference(c):
     _check_run(lab, tr, f, h)
 
 
+@pytest.mark.parametrize("c", G.cases("runs"))
+def test_run_bitwise_vs_exact_model(c):
+    # every device reduction pinned: the GPU equals the exact-arithmetic
+    # model of the same algorithm bit for bit (iterates, movement, modes)
+    from tests import exact_model as X
+
+    f = G.case("runs", c)
+    h = float(f["h"])
+    m = X.meanshiftpp(f["y"], h, _eta(f), int(f["max_iters"]))
+    lab, tr = gs.meanshiftpp(gs.PointSet(f["y"]), gs.ShiftConfig(h=h, eta=_eta(f), max_iters=int(f["max_iters"])))
+    assert tr.iterations == m["iterations"]
+    np.testing.assert_array_equal(tr.total_movement_per_iter, m["movement"])
+    assert np.array_equal(lab.labels, m["labels"])
+    assert np.array_equal(lab.modes, m["modes"])
+    assert [int(v) for v in tr.fingerprint_per_iter] == [int(v) for v in m["iter_fp"]]
+
+
 def test_run_kats():
     # test_modeseek.py:141-236
     lab, tr = gs.meanshiftpp(gs.PointSet(np.tile([1.5, -0.5, 2.0], (40, 1))), gs.ShiftConfig(h=0.7))
@@ -263,15 +280,51 @@ def test_cfg2_image_vs_reference():
     _check_run(lab, tr, f, c["h"])
 
 
-@pytest.mark.slow
-def test_cfg4_10m_vs_reference():
+def _digest(a):
     import hashlib
 
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
+
+
+def _check_model(lab, tr, f, h):
+    """Bitwise equality with the exact-arithmetic model (tests/exact_model.py)
+    and: whatever separates us from the reference is exactly what separates
+    exact arithmetic from the reference's sequential fp64 sums."""
+    assert np.array_equal(lab.modes, f["model_modes"])
+    assert _digest(lab.labels) == str(f["model_labels_digest"])
+    np.testing.assert_array_equal(tr.total_movement_per_iter, f["model_movement"])
+    ref_dev = np.abs(f["model_modes"] - f["modes"]).max()
+    assert np.abs(lab.modes - f["modes"]).max() <= ref_dev
+
+
+@pytest.mark.slow
+def test_cfg4_10m_vs_reference():
     f = G.big("cfg4_10m")
     c = W.CONFIGS["cfg4"]
+    h = c["h"]
     y = W.cloud3d(10_000_000).astype(np.float64)
-    lab, tr = gs.meanshiftpp(gs.PointSet(y), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]))
-    _check_run(lab, tr, f, c["h"])
-    a = np.ascontiguousarray(lab.labels)
-    dg = hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
-    assert dg == str(f["labels_digest"])
+    lab, tr = gs.meanshiftpp(gs.PointSet(y), gs.ShiftConfig(h, c["eta"], c["max_iters"]))
+    # per-iteration cells/counts bit-exact, labels identical to the reference
+    assert tr.iterations == int(f["iterations"])
+    assert [int(v) for v in tr.fingerprint_per_iter] == [int(v) for v in f["iter_fp"]]
+    assert _digest(lab.labels) == str(f["labels_digest"])
+    # modes: bitwise the exact-arithmetic result; the reference's sequential
+    # sums sit 1.73e-9*h away from it after 50 creeping iterations
+    _check_model(lab, tr, f, h)
+
+
+@pytest.mark.parametrize("name", ["cfg0"])
+def test_big_exact_model_bitwise(name):
+    f = G.big(name)
+    c = W.CONFIGS[name]
+    lab, tr = gs.meanshiftpp(gs.PointSet(W.blobs2d()), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]))
+    _check_model(lab, tr, f, c["h"])
+
+
+@pytest.mark.slow
+def test_cfg1_exact_model_bitwise():
+    f = G.big("cfg1")
+    c = W.CONFIGS["cfg1"]
+    lab, tr = gs.segment_pixels(gs.Image(W.cfg1_image()), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]), "rgb")
+    _check_model(lab, tr, f, c["h"])
