@@ -15,7 +15,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libgridshift_cuda.so"
+LIB_PATH = Path(os.environ.get("GRIDSHIFT_LIB", Path(__file__).resolve().parent / "libgridshift_cuda.so"))
 
 GS_OK, GS_EINVAL, GS_ERUNTIME, GS_EUNSUPPORTED = 0, 1, 2, 3
 GS_DTYPE_F64, GS_DTYPE_F32 = 0, 1

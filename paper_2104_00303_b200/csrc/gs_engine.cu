@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -174,6 +175,7 @@ Plan make_plan(int64_t n, int d, double h, const InitStats& s) {
   g.h = h;
   g.d = d;
   g.inv_h = 1.0 / h;
+  if (const char* dbg = getenv("GRIDSHIFT_DEBUG")) g.debug = atoi(dbg);
   __int128 prod = 1;
   double span2 = 0.0;
   int64_t ext[GS_MAXD];

@@ -252,6 +252,10 @@ __global__ void k_soa_to_aos(const double* __restrict__ y, double* __restrict__ 
 
 // --------------------------------------------------------------- k_hist
 
+#ifndef GS_HIST_MINB
+#define GS_HIST_MINB 3
+#endif
+
 // Partial aggregate of a run of points: count and split fixed-point sums.
 template <int D>
 struct Agg {
@@ -303,161 +307,158 @@ __device__ __forceinline__ void flush_segment(const Tab& tab, Ctrl* ctrl, u64 ke
   }
 }
 
-// Warp reduce-by-key: each warp owns a contiguous chunk of 128-point tiles
-// (4 consecutive points per lane).  Per tile: in-lane sequential
+// Fixed-point item of point m of a lane (count 1), or empty.
+template <int D, bool CountOnly>
+__device__ __forceinline__ Agg<D> item_of(const GridParams& g, const double* v, bool valid) {
+  Agg<D> a;
+  a.zero();
+  if (valid) {
+    a.cnt = 1;
+    if constexpr (!CountOnly) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const i64 f = to_fixed(v[j], g.qscale[j]);
+        a.hi[j] = f >> 32;
+        a.lo[j] = (u64)(f & 0xffffffffll);
+      }
+    }
+  }
+  return a;
+}
+
+// Warp reduce-by-key over 128-point tiles (4 consecutive points per lane).
+// Warps take strided super-tiles of S consecutive tiles, so the grid streams
+// through a narrow window of memory, and the segment still open at the end
+// of a tile is carried into the next tile of the super-tile instead of being
+// flushed: a run of one cell costs one flush per S*128 points.  (Hot cells
+// -- a mode can hold ~2% of all points -- otherwise serialise thousands of
+// atomics on one L2 line per iteration.)  Per tile: in-lane sequential
 // aggregation, one segmented inclusive scan of the lane tail aggregates,
 // and every finished segment is flushed once by the lane holding its
-// successor's head.  The open segment at the end of a tile is carried into
-// the next tile (not flushed), so a run of one cell spanning the whole chunk
-// costs one flush: hot cells (a mode can hold ~2% of all points) would
-// otherwise serialise thousands of atomics on one L2 line per iteration.
+// successor's head.  Fast paths: a lane whose 4 points are bitwise
+// identical bins/quantises once; a tile holding one value throughout (every
+// cell-sorted run after iteration 0) skips the scan.  Per-item aggregates
+// are recomputed rather than stored to keep register pressure down.
 template <int D, class Tab, bool CountOnly = false>
-__global__ void __launch_bounds__(kThreads) k_hist(const double* __restrict__ y, i64 n, GridParams g,
+__global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(const double* __restrict__ y, i64 n, GridParams g,
                                                    Tab tab, Ctrl* ctrl, int check_done) {
   if (check_done && *(volatile int*)&ctrl->done) return;
   constexpr int P = 4;
   constexpr int TILE = 32 * P;
+#ifndef GS_HIST_S
+#define GS_HIST_S 8
+#endif
+  constexpr int S = GS_HIST_S;   // tiles per super-tile
   const int lane = threadIdx.x & 31;
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
   const i64 ntiles = (n + TILE - 1) / TILE;
-  const i64 per = (ntiles + nwarps - 1) / nwarps;
-  const i64 t_end = min(ntiles, (warp + 1) * per);
-  u64 ckey = kEmpty;          // carried open segment (uniform across lanes)
-  Agg<D> cagg;
-  cagg.zero();
-  for (i64 tile = warp * per; tile < t_end; ++tile) {
-    const i64 i0 = tile * TILE + P * lane;
-    double v[P][D];
+  const i64 nsuper = (ntiles + S - 1) / S;
+  for (i64 sup = warp; sup < nsuper; sup += nwarps) {
+    u64 ckey = kEmpty;          // carried open segment (uniform across lanes)
+    Agg<D> cagg;
+    cagg.zero();
+    const i64 t_end = min(ntiles, (sup + 1) * S);
+    for (i64 tile = sup * S; tile < t_end; ++tile) {
+      const i64 i0 = tile * TILE + P * lane;
+      double v[P][D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld + i0);
-      const double2 a = __ldcs(src), b = __ldcs(src + 1);
-      v[0][j] = a.x; v[1][j] = a.y; v[2][j] = b.x; v[3][j] = b.y;
-    }
-    // identical consecutive points (every cell-sorted run after iteration
-    // 0) are binned and quantised once: exact, and 4x less arithmetic
-    bool uni = i0 + P - 1 < n;
-#pragma unroll
-    for (int m = 1; m < P; ++m)
-#pragma unroll
-      for (int j = 0; j < D; ++j) uni &= __double_as_longlong(v[m][j]) == __double_as_longlong(v[0][j]);
-    bool same = uni;
-#pragma unroll
-    for (int j = 0; j < D; ++j)
-      same &= __shfl_sync(kFull, __double_as_longlong(v[0][j]), 0) == __double_as_longlong(v[0][j]);
-    if (__all_sync(kFull, same)) {
-      // whole tile one value (all lanes hold it): merge into the carry
-      bool inside;
-      const u64 k0 = pack_key<D>(g, v[0], inside);
-      if (!inside && lane == 0) atomicOr(&ctrl->error, kErrOutOfBox);
-      Agg<D> t;
-      t.zero();
-      t.cnt = TILE;
-      if constexpr (!CountOnly) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const i64 f = to_fixed(v[0][j], g.qscale[j]);
-          t.hi[j] = (f >> 32) * TILE;
-          t.lo[j] = (u64)(f & 0xffffffffll) * TILE;
-        }
+      for (int j = 0; j < D; ++j) {
+        const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld + i0);
+        const double2 a = __ldcs(src), b = __ldcs(src + 1);
+        v[0][j] = a.x; v[1][j] = a.y; v[2][j] = b.x; v[3][j] = b.y;
       }
-      if (k0 == ckey) {
-        cagg.add(t);
+      bool uni = i0 + P - 1 < n;
+#pragma unroll
+      for (int m = 1; m < P; ++m)
+#pragma unroll
+        for (int j = 0; j < D; ++j) uni &= __double_as_longlong(v[m][j]) == __double_as_longlong(v[0][j]);
+      bool same = uni;
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        same &= __shfl_sync(kFull, __double_as_longlong(v[0][j]), 0) == __double_as_longlong(v[0][j]);
+      if (__all_sync(kFull, same)) {
+        // one value throughout the tile (all lanes hold it): merge into the carry
+        bool inside;
+        const u64 k0 = pack_key<D>(g, v[0], inside);
+        if (!inside && lane == 0) atomicOr(&ctrl->error, kErrOutOfBox);
+        Agg<D> t = item_of<D, CountOnly>(g, v[0], true);
+        t.cnt = TILE;
+#pragma unroll
+        for (int j = 0; j < D; ++j) { t.hi[j] *= TILE; t.lo[j] *= TILE; }
+        if (k0 == ckey) {
+          cagg.add(t);
+        } else {
+          if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
+          ckey = k0;
+          cagg = t;
+        }
+        continue;
+      }
+      u64 key[P];
+      if (uni) {
+        bool inside;
+        key[0] = pack_key<D>(g, v[0], inside);
+        if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+#pragma unroll
+        for (int m = 1; m < P; ++m) key[m] = key[0];
       } else {
-        if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
-        ckey = k0;
-        cagg = t;
-      }
-      continue;
-    }
-    u64 key[P];
-    Agg<D> it[P];
 #pragma unroll
-    for (int m = 0; m < P; ++m) {
-      key[m] = kEmpty;
-      it[m].zero();
-    }
-    if (uni) {
-      bool inside;
-      const u64 k0 = pack_key<D>(g, v[0], inside);
-      if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
-#pragma unroll
-      for (int m = 0; m < P; ++m) key[m] = k0;
-      it[0].cnt = P;
-      if constexpr (!CountOnly) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const i64 f = to_fixed(v[0][j], g.qscale[j]);
-          it[0].hi[j] = (f >> 32) * P;
-          it[0].lo[j] = (u64)(f & 0xffffffffll) * P;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int m = 0; m < P; ++m) {
-        if (i0 + m < n) {
-          bool inside;
-          key[m] = pack_key<D>(g, v[m], inside);
-          if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
-          it[m].cnt = 1;
-          if constexpr (!CountOnly) {
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-              const i64 f = to_fixed(v[m][j], g.qscale[j]);
-              it[m].hi[j] = f >> 32;
-              it[m].lo[j] = (u64)(f & 0xffffffffll);
-            }
+        for (int m = 0; m < P; ++m) {
+          key[m] = kEmpty;
+          if (i0 + m < n) {
+            bool inside;
+            key[m] = pack_key<D>(g, v[m], inside);
+            if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
           }
         }
       }
-    }
-    u64 prevkey = __shfl_up_sync(kFull, key[P - 1], 1);
-    if (lane == 0) prevkey = ckey;
-    bool head[P];
-    head[0] = key[0] != prevkey;
+      u64 prevkey = __shfl_up_sync(kFull, key[P - 1], 1);
+      if (lane == 0) prevkey = ckey;
+      bool head[P];
+      head[0] = key[0] != prevkey;
 #pragma unroll
-    for (int m = 1; m < P; ++m) head[m] = key[m] != key[m - 1];
-    // tail aggregate of this lane (items from its last head on); lane 0
-    // starts from the carry when its first item continues it
-    Agg<D> tail;
-    if (lane == 0 && !head[0]) tail = cagg; else tail.zero();
-    bool hashead = false;
+      for (int m = 1; m < P; ++m) head[m] = key[m] != key[m - 1];
+      // tail aggregate of this lane (items from its last head on); lane 0
+      // starts from the carry when its first item continues it
+      Agg<D> x;
+      if (lane == 0 && !head[0]) x = cagg; else x.zero();
+      bool f = false;
 #pragma unroll
-    for (int m = 0; m < P; ++m) {
-      if (head[m]) { tail.zero(); hashead = true; }
-      tail.add(it[m]);
-    }
-    // segmented inclusive scan over lanes: x_L = tail_L + (hashead_L ? 0 : x_{L-1})
-    Agg<D> x = tail;
-    bool f = hashead;
+      for (int m = 0; m < P; ++m) {
+        if (head[m]) { x.zero(); f = true; }
+        x.add(item_of<D, CountOnly>(g, v[m], i0 + m < n));
+      }
+      // segmented inclusive scan over lanes: x_L = tail_L + (hashead_L ? 0 : x_{L-1})
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const Agg<D> yv = x.shfl_up(off);
-      const bool yf = __shfl_up_sync(kFull, f, off);
-      if (lane >= off && !f) { x.add(yv); f = yf; }
-    }
-    Agg<D> acc = x.shfl_up(1);   // open segment carried in from the lanes before
-    if (lane == 0) acc = cagg;
+      for (int off = 1; off < 32; off <<= 1) {
+        const Agg<D> yv = x.shfl_up(off);
+        const bool yf = __shfl_up_sync(kFull, f, off);
+        if (lane >= off && !f) { x.add(yv); f = yf; }
+      }
+      Agg<D> acc = x.shfl_up(1);   // open segment carried in from the lanes before
+      if (lane == 0) acc = cagg;
 #pragma unroll
-    for (int m = 0; m < P; ++m) {
-      if (head[m]) {
-        flush_segment<D, Tab, CountOnly>(tab, ctrl, m ? key[m - 1] : prevkey, acc);
-        acc = it[m];
-      } else {
-        acc.add(it[m]);
+      for (int m = 0; m < P; ++m) {
+        const Agg<D> itm = item_of<D, CountOnly>(g, v[m], i0 + m < n);
+        if (head[m]) {
+          flush_segment<D, Tab, CountOnly>(tab, ctrl, m ? key[m - 1] : prevkey, acc);
+          acc = itm;
+        } else {
+          acc.add(itm);
+        }
+      }
+      // lane 31's open segment becomes the carry
+      ckey = __shfl_sync(kFull, key[P - 1], 31);
+      cagg.cnt = __shfl_sync(kFull, acc.cnt, 31);
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        cagg.hi[j] = (i64)__shfl_sync(kFull, (unsigned long long)acc.hi[j], 31);
+        cagg.lo[j] = __shfl_sync(kFull, acc.lo[j], 31);
       }
     }
-    // lane 31's open segment becomes the carry
-    ckey = __shfl_sync(kFull, key[P - 1], 31);
-    cagg.cnt = __shfl_sync(kFull, acc.cnt, 31);
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      cagg.hi[j] = (i64)__shfl_sync(kFull, (unsigned long long)acc.hi[j], 31);
-      cagg.lo[j] = __shfl_sync(kFull, acc.lo[j], 31);
-    }
+    if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
   }
-  if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
 }
 
 // Dense tables: occupied-cell list from the counts (warp-aggregated append).
