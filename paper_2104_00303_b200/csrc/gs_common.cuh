@@ -58,7 +58,7 @@ struct Ctrl {
   int pad;
   u32 k[2];                // occupied-cell count of the two table buffers
   u32 blocks_done;         // last-block detection for the movement reduction
-  u32 pad2;
+  u32 agg_done;            // last-block detection in k_agg
 };
 
 constexpr int kErrOutOfBox = 1;     // an iterate left the admissible lattice box

@@ -47,9 +47,9 @@ struct Buf {
   size_t cap = 0;
 };
 
-enum Kind { K_INIT = 0, K_HIST, K_AGG, K_SHIFT, K_CLEAR, K_COMP, K_LABELS, K_XPOSE, K_DUMP, K_TRACK,
+enum Kind { K_INIT = 0, K_HIST, K_AGG, K_STEP, K_CLEAR, K_COMP, K_LABELS, K_XPOSE, K_DUMP, K_TRACK,
             K_SORT, K_NKINDS };
-const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "shift", "clear", "components",
+const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "step", "clear", "components",
                                           "labels", "transpose", "dump", "track", "sort"};
 
 constexpr int64_t kSortMinPoints = 1 << 15;   // spatial sort pays off above this
@@ -311,6 +311,17 @@ InitStats run_init(gs_ctx* c, const Input& in, int64_t n, double h, double* y0) 
 
 // -------------------------------------------------------------- iteration
 
+// Histogram of y[0] into table 0 (clean), before the loop.
+template <int D, class Tab>
+void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_pts) {
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  const double* y0 = static_cast<const double*>(c->y[0].p);
+  launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
+}
+
+// Iteration t: table t (buffer t&1) holds the cells of y_t.  k_agg turns it
+// into per-cell target records (and clears buffer (t+1)&1); k_step shifts
+// every point and builds the table of y_{t+1} in the same pass.
 template <int D, class Tab>
 void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, int64_t n, int nb_pts,
                        int nb_cells) {
@@ -318,15 +329,13 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
   double* y_in = static_cast<double*>(c->y[cur].p);
   double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
-  launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, n, p.g, tabs[cur], ctrl, 1); });
-  launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1],
-                                                  static_cast<double*>(c->targets.p), ctrl, cur,
+  Rec<D>* rec = static_cast<Rec<D>*>(c->targets.p);
+  launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur,
                                                   static_cast<u64*>(c->fp_hist.p) + t,
                                                   static_cast<u32*>(c->k_hist.p) + t); });
-  launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur],
-                                                  static_cast<const double*>(c->targets.p), ctrl,
-                                                  static_cast<u64*>(c->partials.p),
-                                                  static_cast<double*>(c->mv_hist.p), t, eta, cur); });
+  launch(c, K_STEP, [&] { k_step<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec,
+                                                  tabs[cur ^ 1], ctrl, static_cast<u64*>(c->partials.p),
+                                                  static_cast<double*>(c->mv_hist.p), t, eta); });
 }
 
 // Occupied-cell list of a table (hash tables maintain theirs on insert;
@@ -353,15 +362,21 @@ void clear_table(gs_ctx* c, const Plan& p, Tab& tab, u32* kp) {
 
 // Extraction of y_final (modeseek.py:256-272).  Table buffer e is clean on
 // entry, buffer e^1 is dirty (cleared here and used as component scratch).
+// `table_ready`: buffer e already holds the table of yf (the last k_step
+// built it); otherwise it is clean and gets built here.
 template <int D, class Tab>
 void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
-                 int64_t* labels_dev, const u32* perm = nullptr) {
+                 int64_t* labels_dev, const u32* perm = nullptr, bool table_ready = false) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
   clear_table<D>(c, p, tabs[e ^ 1], &ctrl->k[e ^ 1]);
-  launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], ctrl, 0); });
-  build_list<D>(c, p, tabs[e]);
+  if (!table_ready)
+    launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], ctrl, 0); });
+  if constexpr (Tab::kDense) {
+    launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e]); });
+    build_list<D>(c, p, tabs[e]);
+  }
   u32* par = ensure<u32>(c, c->par, p.slots);
   u32* first = ensure<u32>(c, c->first, p.slots);
   u32* rankmap = ensure<u32>(c, c->aux, p.slots);
@@ -451,7 +466,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   const InitStats s = run_init<D>(c, in, n, h, y0);
   Plan p = make_plan(n, D, h, s);
   Tabs<D> tabs = make_tabs<D>(c, p);
-  ensure<double>(c, c->targets, p.slots * D);
+  ensure<Rec<D>>(c, c->targets, p.slots);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
@@ -464,6 +479,10 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   const u32* perm = nullptr;
   if (n >= kSortMinPoints)
     perm = p.dense ? spatial_sort<D>(c, p, tabs.dn, n) : spatial_sort<D>(c, p, tabs.hs, n);
+  if (p.dense)
+    enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
+  else
+    enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts);
   // device-driven loop: enqueue chunks, synchronise between chunks only
   int t = 0, chunk = 4;
   while (t < max_iters) {
@@ -486,9 +505,9 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   const int e = r.iters & 1;
   const double* yf = static_cast<const double*>(c->y[e].p);
   if (p.dense)
-    run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev, perm);
+    run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev, perm, true);
   else
-    run_extract<D>(c, p, tabs.hs, yf, n, e, labels_dev, perm);
+    run_extract<D>(c, p, tabs.hs, yf, n, e, labels_dev, perm, true);
   r.k = c->k_last;
   if (movement_out)
     GS_CUDA(cudaMemcpyAsync(movement_out, c->mv_hist.p, sizeof(double) * r.iters, cudaMemcpyDeviceToHost, c->st));
@@ -531,7 +550,7 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   const InitStats s = run_init<D>(c, in, n, h, y0);
   Plan p = make_plan(n, D, h, s);
   Tabs<D> tabs = make_tabs<D>(c, p);
-  ensure<double>(c, c->targets, p.slots * D);
+  ensure<Rec<D>>(c, c->targets, p.slots);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
@@ -541,11 +560,15 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   reset_ctrl(c);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   if (p.dense) {
+    enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
     enqueue_iteration<D>(c, p, tabs.dn, 0, -1.0, n, nb_pts, nb_cells);
     clear_table<D>(c, p, tabs.dn[0], &ctrl->k[0]);
+    clear_table<D>(c, p, tabs.dn[1], &ctrl->k[1]);
   } else {
+    enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts);
     enqueue_iteration<D>(c, p, tabs.hs, 0, -1.0, n, nb_pts, nb_cells);
     clear_table<D>(c, p, tabs.hs[0], &ctrl->k[0]);
+    clear_table<D>(c, p, tabs.hs[1], &ctrl->k[1]);
   }
   double* aos = ensure<double>(c, c->x_stage, (size_t)n * D);
   launch(c, K_XPOSE, [&] { k_soa_to_aos<D><<<nb_pts, kThreads, 0, c->st>>>(y1, aos, n, p.g.ld); });

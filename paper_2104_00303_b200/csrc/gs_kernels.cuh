@@ -326,76 +326,141 @@ __device__ __forceinline__ Agg<D> item_of(const GridParams& g, const double* v, 
   return a;
 }
 
-// Warp reduce-by-key over 128-point tiles (4 consecutive points per lane).
-// Warps take strided super-tiles of S consecutive tiles, so the grid streams
-// through a narrow window of memory, and the segment still open at the end
-// of a tile is carried into the next tile of the super-tile instead of being
-// flushed: a run of one cell costs one flush per S*128 points.  (Hot cells
-// -- a mode can hold ~2% of all points -- otherwise serialise thousands of
-// atomics on one L2 line per iteration.)  Per tile: in-lane sequential
-// aggregation, one segmented inclusive scan of the lane tail aggregates,
-// and every finished segment is flushed once by the lane holding its
-// successor's head.  Fast paths: a lane whose 4 points are bitwise
-// identical bins/quantises once; a tile holding one value throughout (every
-// cell-sorted run after iteration 0) skips the scan.  Per-item aggregates
-// are recomputed rather than stored to keep register pressure down.
+// ---------------------------------------------------------------------------
+// Warp reduce-by-key over one 128-point tile (4 consecutive points per lane):
+// items are (key[m], src[m]) -> count 1 and the fixed-point image of src[m].
+// In-lane sequential aggregation, one segmented inclusive scan of the lane
+// tail aggregates, and every finished segment is flushed once by the lane
+// holding its successor's head.  The segment still open at the end of the
+// tile is carried (ckey, cagg: uniform across lanes) into the next tile of
+// the warp's super-tile instead of being flushed -- a run of one cell costs
+// one flush per super-tile (hot cells: a mode can hold ~2% of all points,
+// and per-tile flushes would serialise thousands of atomics on one L2 line).
+// A tile whose 128 items are identical skips the scan.
+template <int D, class Tab, bool CountOnly>
+__device__ __forceinline__ void rbk_tile(const GridParams& g, const Tab& tab, Ctrl* ctrl, int lane,
+                                         const u64 (&key)[4], const double (&src)[4][D],
+                                         const bool (&valid)[4], bool tile_uniform, u64& ckey,
+                                         Agg<D>& cagg) {
+  constexpr int P = 4;
+  if (tile_uniform) {
+    Agg<D> t = item_of<D, CountOnly>(g, src[0], true);
+    t.cnt = 32 * P;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { t.hi[j] *= 32 * P; t.lo[j] *= 32 * P; }
+    if (key[0] == ckey) {
+      cagg.add(t);
+    } else {
+      if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
+      ckey = key[0];
+      cagg = t;
+    }
+    return;
+  }
+  u64 prevkey = __shfl_up_sync(kFull, key[P - 1], 1);
+  if (lane == 0) prevkey = ckey;
+  bool head[P];
+  head[0] = key[0] != prevkey;
+#pragma unroll
+  for (int m = 1; m < P; ++m) head[m] = key[m] != key[m - 1];
+  // tail aggregate of this lane (items from its last head on); lane 0
+  // starts from the carry when its first item continues it
+  Agg<D> x;
+  if (lane == 0 && !head[0]) x = cagg; else x.zero();
+  bool f = false;
+#pragma unroll
+  for (int m = 0; m < P; ++m) {
+    if (head[m]) { x.zero(); f = true; }
+    x.add(item_of<D, CountOnly>(g, src[m], valid[m]));
+  }
+  // segmented inclusive scan over lanes: x_L = tail_L + (hashead_L ? 0 : x_{L-1})
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Agg<D> yv = x.shfl_up(off);
+    const bool yf = __shfl_up_sync(kFull, f, off);
+    if (lane >= off && !f) { x.add(yv); f = yf; }
+  }
+  Agg<D> acc = x.shfl_up(1);   // open segment carried in from the lanes before
+  if (lane == 0) acc = cagg;
+#pragma unroll
+  for (int m = 0; m < P; ++m) {
+    const Agg<D> itm = item_of<D, CountOnly>(g, src[m], valid[m]);
+    if (head[m]) {
+      flush_segment<D, Tab, CountOnly>(tab, ctrl, m ? key[m - 1] : prevkey, acc);
+      acc = itm;
+    } else {
+      acc.add(itm);
+    }
+  }
+  // lane 31's open segment becomes the carry
+  ckey = __shfl_sync(kFull, key[P - 1], 31);
+  cagg.cnt = __shfl_sync(kFull, acc.cnt, 31);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    cagg.hi[j] = (i64)__shfl_sync(kFull, (unsigned long long)acc.hi[j], 31);
+    cagg.lo[j] = __shfl_sync(kFull, acc.lo[j], 31);
+  }
+}
+
+#ifndef GS_HIST_S
+#define GS_HIST_S 8
+#endif
+constexpr int kSuper = GS_HIST_S;   // tiles per warp super-tile
+
+// Load a lane's 4 consecutive points of tile starting at i0 (SoA, 16-byte
+// vector loads) and classify: `uni` = the lane's 4 points are bitwise
+// identical (and in range), return = every lane of the tile holds the same
+// point (the tile is uniform).
+template <int D>
+__device__ __forceinline__ bool load_quad(const double* __restrict__ y, const GridParams& g, i64 i0, i64 n,
+                                          double (&v)[4][D], bool& uni) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld + i0);
+    const double2 a = __ldcs(src), b = __ldcs(src + 1);
+    v[0][j] = a.x; v[1][j] = a.y; v[2][j] = b.x; v[3][j] = b.y;
+  }
+  uni = i0 + 3 < n;
+#pragma unroll
+  for (int m = 1; m < 4; ++m)
+#pragma unroll
+    for (int j = 0; j < D; ++j) uni &= __double_as_longlong(v[m][j]) == __double_as_longlong(v[0][j]);
+  bool same = uni;
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+    same &= __shfl_sync(kFull, __double_as_longlong(v[0][j]), 0) == __double_as_longlong(v[0][j]);
+  return __all_sync(kFull, same);
+}
+
+// Histogram of one iterate into a clean table (first iteration, extraction
+// of a user-given point set, table dumps; the loop fuses it into k_step).
+// Warps take strided super-tiles of kSuper consecutive 128-point tiles, so
+// the grid streams through a narrow window of memory.
 template <int D, class Tab, bool CountOnly = false>
 __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(const double* __restrict__ y, i64 n, GridParams g,
                                                    Tab tab, Ctrl* ctrl, int check_done) {
   if (check_done && *(volatile int*)&ctrl->done) return;
   constexpr int P = 4;
   constexpr int TILE = 32 * P;
-#ifndef GS_HIST_S
-#define GS_HIST_S 8
-#endif
-  constexpr int S = GS_HIST_S;   // tiles per super-tile
   const int lane = threadIdx.x & 31;
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
   const i64 ntiles = (n + TILE - 1) / TILE;
-  const i64 nsuper = (ntiles + S - 1) / S;
+  const i64 nsuper = (ntiles + kSuper - 1) / kSuper;
   for (i64 sup = warp; sup < nsuper; sup += nwarps) {
-    u64 ckey = kEmpty;          // carried open segment (uniform across lanes)
+    u64 ckey = kEmpty;
     Agg<D> cagg;
     cagg.zero();
-    const i64 t_end = min(ntiles, (sup + 1) * S);
-    for (i64 tile = sup * S; tile < t_end; ++tile) {
+    const i64 t_end = min(ntiles, (sup + 1) * kSuper);
+    for (i64 tile = sup * kSuper; tile < t_end; ++tile) {
       const i64 i0 = tile * TILE + P * lane;
       double v[P][D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld + i0);
-        const double2 a = __ldcs(src), b = __ldcs(src + 1);
-        v[0][j] = a.x; v[1][j] = a.y; v[2][j] = b.x; v[3][j] = b.y;
-      }
-      bool uni = i0 + P - 1 < n;
-#pragma unroll
-      for (int m = 1; m < P; ++m)
-#pragma unroll
-        for (int j = 0; j < D; ++j) uni &= __double_as_longlong(v[m][j]) == __double_as_longlong(v[0][j]);
-      bool same = uni;
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-        same &= __shfl_sync(kFull, __double_as_longlong(v[0][j]), 0) == __double_as_longlong(v[0][j]);
-      if (__all_sync(kFull, same)) {
-        // one value throughout the tile (all lanes hold it): merge into the carry
-        bool inside;
-        const u64 k0 = pack_key<D>(g, v[0], inside);
-        if (!inside && lane == 0) atomicOr(&ctrl->error, kErrOutOfBox);
-        Agg<D> t = item_of<D, CountOnly>(g, v[0], true);
-        t.cnt = TILE;
-#pragma unroll
-        for (int j = 0; j < D; ++j) { t.hi[j] *= TILE; t.lo[j] *= TILE; }
-        if (k0 == ckey) {
-          cagg.add(t);
-        } else {
-          if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
-          ckey = k0;
-          cagg = t;
-        }
-        continue;
-      }
+      bool uni;
+      const bool tu = load_quad<D>(y, g, i0, n, v, uni);
       u64 key[P];
+      bool valid[P];
+#pragma unroll
+      for (int m = 0; m < P; ++m) valid[m] = i0 + m < n;
       if (uni) {
         bool inside;
         key[0] = pack_key<D>(g, v[0], inside);
@@ -406,58 +471,173 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(
 #pragma unroll
         for (int m = 0; m < P; ++m) {
           key[m] = kEmpty;
-          if (i0 + m < n) {
+          if (valid[m]) {
             bool inside;
             key[m] = pack_key<D>(g, v[m], inside);
             if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
           }
         }
       }
-      u64 prevkey = __shfl_up_sync(kFull, key[P - 1], 1);
-      if (lane == 0) prevkey = ckey;
-      bool head[P];
-      head[0] = key[0] != prevkey;
-#pragma unroll
-      for (int m = 1; m < P; ++m) head[m] = key[m] != key[m - 1];
-      // tail aggregate of this lane (items from its last head on); lane 0
-      // starts from the carry when its first item continues it
-      Agg<D> x;
-      if (lane == 0 && !head[0]) x = cagg; else x.zero();
-      bool f = false;
-#pragma unroll
-      for (int m = 0; m < P; ++m) {
-        if (head[m]) { x.zero(); f = true; }
-        x.add(item_of<D, CountOnly>(g, v[m], i0 + m < n));
-      }
-      // segmented inclusive scan over lanes: x_L = tail_L + (hashead_L ? 0 : x_{L-1})
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const Agg<D> yv = x.shfl_up(off);
-        const bool yf = __shfl_up_sync(kFull, f, off);
-        if (lane >= off && !f) { x.add(yv); f = yf; }
-      }
-      Agg<D> acc = x.shfl_up(1);   // open segment carried in from the lanes before
-      if (lane == 0) acc = cagg;
-#pragma unroll
-      for (int m = 0; m < P; ++m) {
-        const Agg<D> itm = item_of<D, CountOnly>(g, v[m], i0 + m < n);
-        if (head[m]) {
-          flush_segment<D, Tab, CountOnly>(tab, ctrl, m ? key[m - 1] : prevkey, acc);
-          acc = itm;
-        } else {
-          acc.add(itm);
-        }
-      }
-      // lane 31's open segment becomes the carry
-      ckey = __shfl_sync(kFull, key[P - 1], 31);
-      cagg.cnt = __shfl_sync(kFull, acc.cnt, 31);
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        cagg.hi[j] = (i64)__shfl_sync(kFull, (unsigned long long)acc.hi[j], 31);
-        cagg.lo[j] = __shfl_sync(kFull, acc.lo[j], 31);
-      }
+      rbk_tile<D, Tab, CountOnly>(g, tab, ctrl, lane, key, v, valid, tu, ckey, cagg);
     }
     if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
+  }
+}
+
+// Cell record written by k_agg: the target (the cell's 3^d-neighbourhood
+// mean, D doubles) followed by the packed key of the target's own cell.
+template <int D>
+struct Rec {
+  double t[D];
+  u64 key;
+};
+
+// Movement of one point, as a 128-bit fixed-point increment.
+template <int D>
+__device__ __forceinline__ u128 move_fixed(const GridParams& g, const double* t, const double* v) {
+  double sq[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double dlt = __dsub_rn(t[j], v[j]);
+    sq[j] = __dmul_rn(dlt, dlt);
+  }
+  return norm_to_fixed(__dsqrt_rn(row_sum<D>(sq)), g.movement_exp);
+}
+
+template <int D, class Tab>
+__device__ __forceinline__ const Rec<D>& lookup_rec(const GridParams& g, const Tab& tab, const Rec<D>* rec,
+                                                    const double* v, Ctrl* ctrl) {
+  bool inside;
+  const u64 key = pack_key<D>(g, v, inside);
+  u32 s = 0;
+  if constexpr (Tab::kDense) {
+    if (inside) s = (u32)key; else atomicOr(&ctrl->error, kErrMissing);
+  } else {
+    if (!inside || !tab.find(key, s)) { atomicOr(&ctrl->error, kErrMissing); s = 0; }
+  }
+  return rec[s];
+}
+
+// The fused iteration kernel: shift of iteration t (modeseek.py:109-110)
+// and the histogram of iteration t+1 (grid.py:179-190) in one pass over the
+// points.  Per 128-point tile: load y, look up each point's cell record,
+// store y' = target, accumulate the movement, and reduce-by-key the targets'
+// cells straight into the next table (y' never leaves registers).  Points
+// with bitwise-identical inputs share one lookup/norm (exact: identical
+// inputs give identical outputs, and the movement is scaled in fixed point).
+// The last CTA finishes the movement reduction and evaluates
+// `movement < eta` (modeseek.py:139) on device.
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_step(
+    const double* __restrict__ y, double* __restrict__ yo, i64 n, GridParams g, Tab cur,
+    const Rec<D>* __restrict__ rec, Tab nxt, Ctrl* ctrl, u64* partials, double* mv_hist, int t,
+    double eta) {
+  if (*(volatile int*)&ctrl->done) return;
+  constexpr int P = 4;
+  constexpr int TILE = 32 * P;
+  const int lane = threadIdx.x & 31;
+  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  const i64 ntiles = (n + TILE - 1) / TILE;
+  const i64 nsuper = (ntiles + kSuper - 1) / kSuper;
+  u64 ahi = 0, alo = 0;
+  for (i64 sup = warp; sup < nsuper; sup += nwarps) {
+    u64 ckey = kEmpty;
+    Agg<D> cagg;
+    cagg.zero();
+    const i64 t_end = min(ntiles, (sup + 1) * kSuper);
+    for (i64 tile = sup * kSuper; tile < t_end; ++tile) {
+      const i64 i0 = tile * TILE + P * lane;
+      double v[P][D];
+      bool uni;
+      const bool tu = load_quad<D>(y, g, i0, n, v, uni);
+      double o[P][D];
+      u64 key[P];
+      bool valid[P];
+#pragma unroll
+      for (int m = 0; m < P; ++m) valid[m] = i0 + m < n;
+      if (uni) {
+        const Rec<D>& r = lookup_rec<D>(g, cur, rec, v[0], ctrl);
+        double tt[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) tt[j] = r.t[j];
+        const u64 kk = r.key;
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+          key[m] = kk;
+#pragma unroll
+          for (int j = 0; j < D; ++j) o[m][j] = tt[j];
+        }
+        const u128 f = move_fixed<D>(g, tt, v[0]) << 2;
+        add128(ahi, alo, (u64)(f >> 64), (u64)f);
+      } else {
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+          key[m] = kEmpty;
+          if (valid[m]) {
+            const Rec<D>& r = lookup_rec<D>(g, cur, rec, v[m], ctrl);
+#pragma unroll
+            for (int j = 0; j < D; ++j) o[m][j] = r.t[j];
+            key[m] = r.key;
+            const u128 f = move_fixed<D>(g, o[m], v[m]);
+            add128(ahi, alo, (u64)(f >> 64), (u64)f);
+          } else {
+#pragma unroll
+            for (int j = 0; j < D; ++j) o[m][j] = v[m][j];
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double2* dst = reinterpret_cast<double2*>(yo + (i64)j * g.ld + i0);
+        __stcs(dst, make_double2(o[0][j], o[1][j]));
+        __stcs(dst + 1, make_double2(o[2][j], o[3][j]));
+      }
+      rbk_tile<D, Tab, false>(g, nxt, ctrl, lane, key, o, valid, tu, ckey, cagg);
+    }
+    if (lane == 0) flush_segment<D, Tab, false>(nxt, ctrl, ckey, cagg);
+  }
+  // block reduction of the 128-bit movement, last CTA finishes
+  for (int off = 16; off; off >>= 1) {
+    const u64 oh = __shfl_xor_sync(kFull, ahi, off);
+    const u64 ol = __shfl_xor_sync(kFull, alo, off);
+    add128(ahi, alo, oh, ol);
+  }
+  __shared__ u64 sh[kThreads / 32][2];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5;
+  if (lane == 0) { sh[w][0] = ahi; sh[w][1] = alo; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 bh = 0, bl = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    partials[2 * blockIdx.x] = bh;
+    partials[2 * blockIdx.x + 1] = bl;
+    __threadfence();
+    const u32 ticket = atomicAdd(&ctrl->blocks_done, 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  u64 th = 0, tl = 0;
+  for (u32 b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+    add128(th, tl, __ldcg(partials + 2 * b), __ldcg(partials + 2 * b + 1));
+  for (int off = 16; off; off >>= 1) {
+    const u64 oh = __shfl_xor_sync(kFull, th, off);
+    const u64 ol = __shfl_xor_sync(kFull, tl, off);
+    add128(th, tl, oh, ol);
+  }
+  __syncthreads();
+  if (lane == 0) { sh[w][0] = th; sh[w][1] = tl; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 bh = 0, bl = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
+    mv_hist[t] = mv;
+    ctrl->iters = t + 1;
+    ctrl->blocks_done = 0;
+    if (mv < eta) ctrl->done = 1;
   }
 }
 
@@ -521,24 +701,30 @@ __device__ __forceinline__ void neighbourhood_sum(const GridParams& g, const Tab
 }
 
 template <int D, class Tab>
-__device__ __forceinline__ void agg_cell(const GridParams& g, const Tab& tab, u32 s, double* __restrict__ targets,
-                                         u64& fp) {
+__device__ __forceinline__ void agg_cell(const GridParams& g, const Tab& tab, u32 s, Rec<D>* __restrict__ rec,
+                                         u64& fp, Ctrl* ctrl) {
   const u64 key = tab.key_of(s);
   u64 cnt;
   i128 sum[D];
   neighbourhood_sum<D>(g, tab, key, cnt, sum);
   const double c = (double)cnt;
+  Rec<D> r;
 #pragma unroll
-  for (int j = 0; j < D; ++j) targets[(i64)s * D + j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
+  for (int j = 0; j < D; ++j) r.t[j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
+  bool inside;
+  r.key = pack_key<D>(g, r.t, inside);
+  if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+  rec[s] = r;
   fp += cell_fingerprint<D>(g, key, tab.ent[s].count);
 }
 
-// Per occupied cell: 3^d neighbourhood -> target mean.  Dense tables are
+// Per occupied cell: 3^d neighbourhood -> target record.  Dense tables are
 // walked slot by slot (empty slots are one 8-byte read); hash tables by
-// their occupied list.  Also clears the previous iteration's table and
-// records k and the (cells, counts) fingerprint of this iteration.
+// their occupied list.  Also clears the previous iteration's table (the
+// next k_step fills it) and records k and the (cells, counts) fingerprint
+// of this iteration; the last CTA resets the cleared table's cell count.
 template <int D, class Tab>
-__global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab prev, double* __restrict__ targets,
+__global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab prev, Rec<D>* __restrict__ rec,
                                                   Ctrl* ctrl, int cur, u64* fp_out, u32* k_out) {
   if (*(volatile int*)&ctrl->done) return;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -557,7 +743,7 @@ __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab pre
     }
     for (i64 s = tid; s < ns; s += stride) {
       if (tab.ent[s].count == 0) continue;
-      agg_cell<D>(g, tab, (u32)s, targets, fp);
+      agg_cell<D>(g, tab, (u32)s, rec, fp, ctrl);
       ++kc;
     }
   } else {
@@ -572,7 +758,7 @@ __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab pre
     }
     const u32 k = ctrl->k[cur];
     for (i64 a = tid; a < k; a += stride) {
-      agg_cell<D>(g, tab, tab.list[a], targets, fp);
+      agg_cell<D>(g, tab, tab.list[a], rec, fp, ctrl);
       ++kc;
     }
   }
@@ -584,135 +770,13 @@ __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab pre
     if (fp) atomicAdd((unsigned long long*)fp_out, (unsigned long long)fp);
     if (kc) atomicAdd(k_out, kc);
   }
-}
-
-// -------------------------------------------------------------- k_shift
-
-template <int D, class Tab>
-__device__ __forceinline__ double shift_point(const GridParams& g, const Tab& tab,
-                                              const double* __restrict__ targets, const double* v,
-                                              double* out, Ctrl* ctrl) {
-  bool inside;
-  const u64 key = pack_key<D>(g, v, inside);
-  u32 s;
-  if constexpr (Tab::kDense) {
-    s = (u32)key;
-    if (!inside) { atomicOr(&ctrl->error, kErrMissing); s = 0; }
-  } else {
-    if (!inside || !tab.find(key, s)) { atomicOr(&ctrl->error, kErrMissing); s = 0; }
-  }
-  double sq[D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    out[j] = __ldg(targets + (i64)s * D + j);
-    const double dlt = __dsub_rn(out[j], v[j]);
-    sq[j] = __dmul_rn(dlt, dlt);
-  }
-  return __dsqrt_rn(row_sum<D>(sq));
-}
-
-// Four consecutive points per thread and loop trip (two 16-byte vector
-// loads per SoA axis); streaming loads/stores keep the cell tables in L2.
-template <int D, class Tab>
-__global__ void __launch_bounds__(kThreads, 3) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
-                                                    GridParams g, Tab tab, const double* __restrict__ targets,
-                                                    Ctrl* ctrl, u64* partials, double* mv_hist, int t,
-                                                    double eta, int cur) {
-  if (*(volatile int*)&ctrl->done) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->k[cur ^ 1] = 0;
-  u64 ahi = 0, alo = 0;
-  const i64 stride = (i64)gridDim.x * blockDim.x;
-  const i64 nquads = (n + 3) >> 2;
-  for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < nquads; q += stride) {
-    double2 in[D][2];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld) + 2 * q;
-      in[j][0] = __ldcs(src);
-      in[j][1] = __ldcs(src + 1);
-    }
-    double out[4][D];
-    bool uni = 4 * q + 3 < n;
-#pragma unroll
-    for (int j = 0; j < D; ++j)
-      uni &= (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][0].y)) &
-             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].x)) &
-             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].y));
-    if (uni) {
-      // four identical points: one lookup, one norm, movement x4 (exact)
-      double v[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = in[j][0].x;
-      const double mv = shift_point<D>(g, tab, targets, v, out[0], ctrl);
-      const u128 f = norm_to_fixed(mv, g.movement_exp) << 2;
-      add128(ahi, alo, (u64)(f >> 64), (u64)f);
-#pragma unroll
-      for (int j = 0; j < D; ++j) out[1][j] = out[2][j] = out[3][j] = out[0][j];
-    } else {
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        double v[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) v[j] = (m & 1) ? in[j][m >> 1].y : in[j][m >> 1].x;
-        if (4 * q + m < n) {
-          const double mv = shift_point<D>(g, tab, targets, v, out[m], ctrl);
-          const u128 f = norm_to_fixed(mv, g.movement_exp);
-          add128(ahi, alo, (u64)(f >> 64), (u64)f);
-        } else {
-#pragma unroll
-          for (int j = 0; j < D; ++j) out[m][j] = v[j];
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      double2* dst = reinterpret_cast<double2*>(yo + (i64)j * g.ld) + 2 * q;
-      __stcs(dst, make_double2(out[0][j], out[1][j]));
-      __stcs(dst + 1, make_double2(out[2][j], out[3][j]));
-    }
-  }
-  // block reduction of the 128-bit movement
-  for (int o = 16; o; o >>= 1) {
-    const u64 oh = __shfl_xor_sync(kFull, ahi, o);
-    const u64 ol = __shfl_xor_sync(kFull, alo, o);
-    add128(ahi, alo, oh, ol);
-  }
-  __shared__ u64 sh[kThreads / 32][2];
-  __shared__ bool last;
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) { sh[w][0] = ahi; sh[w][1] = alo; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    u64 bh = 0, bl = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
-    partials[2 * blockIdx.x] = bh;
-    partials[2 * blockIdx.x + 1] = bl;
     __threadfence();
-    const u32 ticket = atomicAdd(&ctrl->blocks_done, 1u);
-    last = (ticket == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  // last CTA: fixed-order reduction over the partials
-  u64 th = 0, tl = 0;
-  for (u32 b = threadIdx.x; b < gridDim.x; b += blockDim.x)
-    add128(th, tl, __ldcg(partials + 2 * b), __ldcg(partials + 2 * b + 1));
-  for (int o = 16; o; o >>= 1) {
-    const u64 oh = __shfl_xor_sync(kFull, th, o);
-    const u64 ol = __shfl_xor_sync(kFull, tl, o);
-    add128(th, tl, oh, ol);
-  }
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) { sh[w][0] = th; sh[w][1] = tl; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    u64 bh = 0, bl = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
-    const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
-    mv_hist[t] = mv;
-    ctrl->iters = t + 1;
-    ctrl->blocks_done = 0;
-    if (mv < eta) ctrl->done = 1;
+    if (atomicAdd(&ctrl->agg_done, 1u) == gridDim.x - 1) {
+      ctrl->k[cur ^ 1] = 0;   // every CTA has read it: the next k_step appends from 0
+      ctrl->agg_done = 0;
+    }
   }
 }
 
