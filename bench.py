@@ -261,11 +261,11 @@ def our_arm(a):
     # roofline of the dominant per-point kernel
     n_local = x_dev.shape[0]
     d = 3
-    # k_step = shift of iteration t fused with the histogram of t+1: reads y,
-    # writes y' (16*d B/point); k_hist runs once per step on the input
-    bytes_per = {"hist": 8 * d * n_local, "step": 16 * d * n_local}
-    work = {"hist": a.steps, "step": iters_total}
-    kern = max(("hist", "step", "agg"), key=lambda k: prof[k][0])
+    # k_shift reads y and writes y' (16*d B/point); k_hist bins the input
+    # once per step (later tables are derived per cell, k_derive)
+    bytes_per = {"hist": 8 * d * n_local, "shift": 16 * d * n_local}
+    work = {"hist": a.steps, "shift": iters_total}
+    kern = max(("hist", "shift", "agg"), key=lambda k: prof[k][0])
     peak, peak_src = measured_peak()
     roof = None
     if kern in bytes_per:
@@ -277,7 +277,7 @@ def our_arm(a):
                 "alg_bytes_per_launch": bytes_per[kern],
                 "avg_launch_ms": prof[kern][0] / work[kern], "traffic_source": tsrc}
     kernels = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
-    for k in ("hist", "step"):
+    for k in ("hist", "shift"):
         if k in kernels and prof[k][0] > 0:
             kernels[k]["achieved_gbs"] = bytes_per[k] * work[k] / (prof[k][0] / 1e3) / 1e9
     launches = int(sum(v[1] for v in prof.values()))

@@ -111,7 +111,7 @@ def ref(x):
     return C.byref(x)
 
 
-N_KINDS = 11
+N_KINDS = 12
 
 
 def profile(mode: int, device: int | None = None):

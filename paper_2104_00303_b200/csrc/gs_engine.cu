@@ -47,10 +47,10 @@ struct Buf {
   size_t cap = 0;
 };
 
-enum Kind { K_INIT = 0, K_HIST, K_AGG, K_STEP, K_CLEAR, K_COMP, K_LABELS, K_XPOSE, K_DUMP, K_TRACK,
-            K_SORT, K_NKINDS };
-const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "step", "clear", "components",
-                                          "labels", "transpose", "dump", "track", "sort"};
+enum Kind { K_INIT = 0, K_HIST, K_AGG, K_SHIFT, K_CLEAR, K_COMP, K_LABELS, K_XPOSE, K_DUMP, K_TRACK,
+            K_SORT, K_DERIVE, K_NKINDS };
+const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "shift", "clear", "components",
+                                          "labels", "transpose", "dump", "track", "sort", "derive"};
 
 constexpr int64_t kSortMinPoints = 1 << 15;   // spatial sort pays off above this
 
@@ -320,8 +320,8 @@ void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_p
 }
 
 // Iteration t: table t (buffer t&1) holds the cells of y_t.  k_agg turns it
-// into per-cell target records (and clears buffer (t+1)&1); k_step shifts
-// every point and builds the table of y_{t+1} in the same pass.
+// into per-cell target records (and clears buffer (t+1)&1), k_derive builds
+// the table of y_{t+1} from it (O(cells)), k_shift moves every point.
 template <int D, class Tab>
 void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, int64_t n, int nb_pts,
                        int nb_cells) {
@@ -333,8 +333,10 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
   launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur,
                                                   static_cast<u64*>(c->fp_hist.p) + t,
                                                   static_cast<u32*>(c->k_hist.p) + t); });
-  launch(c, K_STEP, [&] { k_step<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec,
-                                                  tabs[cur ^ 1], ctrl, static_cast<u64*>(c->partials.p),
+  launch(c, K_DERIVE, [&] { k_derive<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
+                                                                                ctrl, cur); });
+  launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec, ctrl,
+                                                  static_cast<u64*>(c->partials.p),
                                                   static_cast<double*>(c->mv_hist.p), t, eta); });
 }
 

@@ -518,86 +518,76 @@ __device__ __forceinline__ const Rec<D>& lookup_rec(const GridParams& g, const T
   return rec[s];
 }
 
-// The fused iteration kernel: shift of iteration t (modeseek.py:109-110)
-// and the histogram of iteration t+1 (grid.py:179-190) in one pass over the
-// points.  Per 128-point tile: load y, look up each point's cell record,
-// store y' = target, accumulate the movement, and reduce-by-key the targets'
-// cells straight into the next table (y' never leaves registers).  Points
-// with bitwise-identical inputs share one lookup/norm (exact: identical
-// inputs give identical outputs, and the movement is scaled in fixed point).
-// The last CTA finishes the movement reduction and evaluates
-// `movement < eta` (modeseek.py:139) on device.
+// Shift of iteration t (modeseek.py:109-110): per 4-point quad (two 16-byte
+// vector loads per SoA axis) look up the cell record, write y' = target,
+// accumulate the per-point L2 movement in 128-bit fixed point.  Quads of
+// bitwise-identical points (every cell-sorted run after iteration 0) share
+// one lookup and one norm (exact: identical inputs, movement scaled by 4 in
+// fixed point).  Streaming loads/stores keep the tables in L2.  The last CTA
+// finishes the movement reduction and evaluates `movement < eta`
+// (modeseek.py:139) on device.
 template <int D, class Tab>
-__global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_step(
-    const double* __restrict__ y, double* __restrict__ yo, i64 n, GridParams g, Tab cur,
-    const Rec<D>* __restrict__ rec, Tab nxt, Ctrl* ctrl, u64* partials, double* mv_hist, int t,
-    double eta) {
+__global__ void __launch_bounds__(kThreads, 3) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
+                                                       GridParams g, Tab tab, const Rec<D>* __restrict__ rec,
+                                                       Ctrl* ctrl, u64* partials, double* mv_hist, int t,
+                                                       double eta) {
   if (*(volatile int*)&ctrl->done) return;
-  constexpr int P = 4;
-  constexpr int TILE = 32 * P;
-  const int lane = threadIdx.x & 31;
-  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  const i64 ntiles = (n + TILE - 1) / TILE;
-  const i64 nsuper = (ntiles + kSuper - 1) / kSuper;
   u64 ahi = 0, alo = 0;
-  for (i64 sup = warp; sup < nsuper; sup += nwarps) {
-    u64 ckey = kEmpty;
-    Agg<D> cagg;
-    cagg.zero();
-    const i64 t_end = min(ntiles, (sup + 1) * kSuper);
-    for (i64 tile = sup * kSuper; tile < t_end; ++tile) {
-      const i64 i0 = tile * TILE + P * lane;
-      double v[P][D];
-      bool uni;
-      const bool tu = load_quad<D>(y, g, i0, n, v, uni);
-      double o[P][D];
-      u64 key[P];
-      bool valid[P];
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 nquads = (n + 3) >> 2;
+  for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < nquads; q += stride) {
+    double2 in[D][2];
 #pragma unroll
-      for (int m = 0; m < P; ++m) valid[m] = i0 + m < n;
-      if (uni) {
-        const Rec<D>& r = lookup_rec<D>(g, cur, rec, v[0], ctrl);
-        double tt[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) tt[j] = r.t[j];
-        const u64 kk = r.key;
-#pragma unroll
-        for (int m = 0; m < P; ++m) {
-          key[m] = kk;
-#pragma unroll
-          for (int j = 0; j < D; ++j) o[m][j] = tt[j];
-        }
-        const u128 f = move_fixed<D>(g, tt, v[0]) << 2;
-        add128(ahi, alo, (u64)(f >> 64), (u64)f);
-      } else {
-#pragma unroll
-        for (int m = 0; m < P; ++m) {
-          key[m] = kEmpty;
-          if (valid[m]) {
-            const Rec<D>& r = lookup_rec<D>(g, cur, rec, v[m], ctrl);
-#pragma unroll
-            for (int j = 0; j < D; ++j) o[m][j] = r.t[j];
-            key[m] = r.key;
-            const u128 f = move_fixed<D>(g, o[m], v[m]);
-            add128(ahi, alo, (u64)(f >> 64), (u64)f);
-          } else {
-#pragma unroll
-            for (int j = 0; j < D; ++j) o[m][j] = v[m][j];
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        double2* dst = reinterpret_cast<double2*>(yo + (i64)j * g.ld + i0);
-        __stcs(dst, make_double2(o[0][j], o[1][j]));
-        __stcs(dst + 1, make_double2(o[2][j], o[3][j]));
-      }
-      rbk_tile<D, Tab, false>(g, nxt, ctrl, lane, key, o, valid, tu, ckey, cagg);
+    for (int j = 0; j < D; ++j) {
+      const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld) + 2 * q;
+      in[j][0] = __ldcs(src);
+      in[j][1] = __ldcs(src + 1);
     }
-    if (lane == 0) flush_segment<D, Tab, false>(nxt, ctrl, ckey, cagg);
+    double out[4][D];
+    bool uni = 4 * q + 3 < n;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      uni &= (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][0].y)) &
+             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].x)) &
+             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].y));
+    if (uni) {
+      double v[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = in[j][0].x;
+      const Rec<D>& r = lookup_rec<D>(g, tab, rec, v, ctrl);
+#pragma unroll
+      for (int j = 0; j < D; ++j) out[0][j] = r.t[j];
+      const u128 f = move_fixed<D>(g, out[0], v) << 2;
+      add128(ahi, alo, (u64)(f >> 64), (u64)f);
+#pragma unroll
+      for (int j = 0; j < D; ++j) out[1][j] = out[2][j] = out[3][j] = out[0][j];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        double v[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) v[j] = (m & 1) ? in[j][m >> 1].y : in[j][m >> 1].x;
+        if (4 * q + m < n) {
+          const Rec<D>& r = lookup_rec<D>(g, tab, rec, v, ctrl);
+#pragma unroll
+          for (int j = 0; j < D; ++j) out[m][j] = r.t[j];
+          const u128 f = move_fixed<D>(g, out[m], v);
+          add128(ahi, alo, (u64)(f >> 64), (u64)f);
+        } else {
+#pragma unroll
+          for (int j = 0; j < D; ++j) out[m][j] = v[j];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double2* dst = reinterpret_cast<double2*>(yo + (i64)j * g.ld) + 2 * q;
+      __stcs(dst, make_double2(out[0][j], out[1][j]));
+      __stcs(dst + 1, make_double2(out[2][j], out[3][j]));
+    }
   }
   // block reduction of the 128-bit movement, last CTA finishes
+  const int lane = threadIdx.x & 31;
   for (int off = 16; off; off >>= 1) {
     const u64 oh = __shfl_xor_sync(kFull, ahi, off);
     const u64 ol = __shfl_xor_sync(kFull, alo, off);
@@ -610,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_step(
   __syncthreads();
   if (threadIdx.x == 0) {
     u64 bh = 0, bl = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    for (int qq = 0; qq < (int)(blockDim.x >> 5); ++qq) add128(bh, bl, sh[qq][0], sh[qq][1]);
     partials[2 * blockIdx.x] = bh;
     partials[2 * blockIdx.x + 1] = bl;
     __threadfence();
@@ -632,12 +622,44 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_step(
   __syncthreads();
   if (threadIdx.x == 0) {
     u64 bh = 0, bl = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    for (int qq = 0; qq < (int)(blockDim.x >> 5); ++qq) add128(bh, bl, sh[qq][0], sh[qq][1]);
     const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
     mv_hist[t] = mv;
     ctrl->iters = t + 1;
     ctrl->blocks_done = 0;
     if (mv < eta) ctrl->done = 1;
+  }
+}
+
+// Table of y_{t+1} from the table of y_t.  Every point of occupied cell c
+// moves to exactly target_c (modeseek.py:109: y' depends on the cell only),
+// so the per-point histogram of y_{t+1} (grid.py:179-190) equals
+//     count[key(target_c)] += count_c,  sums[key(target_c)] += count_c * fixed(target_c)
+// summed over c -- an identity over integers, hence bit-identical to binning
+// the points (tests: per-iteration fingerprints and the exact model).
+// Dense tables are walked in key order (adjacent cells tend to share a
+// target cell); the buffer receiving the new table was cleared by k_agg.
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_derive(GridParams g, Tab cur, Tab nxt, const Rec<D>* __restrict__ rec,
+                                                     Ctrl* ctrl, int c) {
+  if (*(volatile int*)&ctrl->done) return;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  const i64 items = Tab::kDense ? (i64)g.nkeys : (i64)ctrl->k[c];
+  for (i64 a = tid; a < items; a += stride) {
+    const u32 s = Tab::kDense ? (u32)a : cur.list[a];
+    const u64 cnt = cur.ent[s].count;
+    if (cnt == 0) continue;
+    const Rec<D> r = rec[s];
+    Agg<D> ag;
+    ag.cnt = (u32)cnt;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const i64 f = to_fixed(r.t[j], g.qscale[j]);
+      ag.hi[j] = (f >> 32) * (i64)cnt;
+      ag.lo[j] = (u64)(f & 0xffffffffll) * cnt;
+    }
+    flush_segment<D, Tab, false>(nxt, ctrl, r.key, ag);
   }
 }
 
