@@ -59,6 +59,8 @@ struct Ctrl {
   u32 k[2];                // occupied-cell count of the two table buffers
   u32 blocks_done;         // last-block detection for the movement reduction
   u32 agg_done;            // last-block detection in k_agg
+  u32 nruns;               // initial cells (runs) after the spatial sort
+  u32 pad3;
 };
 
 constexpr int kErrOutOfBox = 1;     // an iterate left the admissible lattice box

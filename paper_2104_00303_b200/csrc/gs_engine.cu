@@ -77,7 +77,7 @@ struct gs_ctx {
   // device buffers
   Buf x_stage, y[2], ent[2], keys[2], list[2], targets, partials, par, first, aux, roots,
       root_first, ranks, modes, labels, mv_hist, fp_hist, k_hist, stats, ctrl, perm, track,
-      track_out, bitmaps, scan;
+      track_out, bitmaps, scan, runoff, runstart, runmin, runlist, cell0;
   // pinned host mirrors
   Ctrl* h_ctrl = nullptr;
   InitStats* h_stats = nullptr;
@@ -309,6 +309,15 @@ InitStats run_init(gs_ctx* c, const Input& in, int64_t n, double h, double* y0) 
   return *c->h_stats;
 }
 
+// What the spatial sort leaves behind for the run-based extraction.
+struct SortInfo {
+  u32* cell0 = nullptr;     // initial cell slot per point, original order
+  u32* start = nullptr;     // per initial slot: run start in sorted order
+  u32* minidx = nullptr;    // per initial slot: smallest original index
+  u32* runs = nullptr;      // occupied initial slots
+  u32* runroot = nullptr;   // per initial slot: final component root (scratch)
+};
+
 // -------------------------------------------------------------- iteration
 
 // Histogram of y[0] into table 0 (clean), before the loop.
@@ -368,7 +377,7 @@ void clear_table(gs_ctx* c, const Plan& p, Tab& tab, u32* kp) {
 // built it); otherwise it is clean and gets built here.
 template <int D, class Tab>
 void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
-                 int64_t* labels_dev, const u32* perm = nullptr, bool table_ready = false) {
+                 int64_t* labels_dev, const SortInfo* si = nullptr, bool table_ready = false) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
@@ -388,7 +397,13 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
   launch(c, K_COMP, [&] { k_uf_init<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first); });
   launch(c, K_COMP, [&] { k_uf_link<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[e], &ctrl->k[e], par); });
   launch(c, K_COMP, [&] { k_uf_flatten<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, tabs[e ^ 1].ent); });
-  launch(c, K_LABELS, [&] { k_first<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, first, perm, ctrl); });
+  if (si)
+    launch(c, K_LABELS, [&] {
+      k_run_first<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(yf, p.g, tabs[e], si->runs, &ctrl->nruns, si->start,
+                                                            si->minidx, par, first, si->runroot, ctrl);
+    });
+  else
+    launch(c, K_LABELS, [&] { k_first<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, first, nullptr, ctrl); });
   GS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(u32), c->st));
   launch(c, K_COMP, [&] { k_roots<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first, roots, rfirst, nroots); });
   check_launch();
@@ -413,7 +428,12 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
   GS_CUDA(cudaMemcpyAsync(dranks, rk.data(), nr * sizeof(u32), cudaMemcpyHostToDevice, c->st));
   double* dmodes = ensure<double>(c, c->modes, (size_t)nr * D + 1);
   launch(c, K_COMP, [&] { k_modes<D><<<blocks_for(c, nr), kThreads, 0, c->st>>>(p.g, roots, dranks, nr, rankmap, tabs[e ^ 1].ent, dmodes); });
-  launch(c, K_LABELS, [&] { k_labels<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, rankmap, perm,
+  if (si)
+    launch(c, K_LABELS, [&] {
+      k_labels_runs<<<nb_pts, kThreads, 0, c->st>>>(si->cell0, n, si->runroot, rankmap, reinterpret_cast<i64*>(labels_dev));
+    });
+  else
+    launch(c, K_LABELS, [&] { k_labels<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, rankmap, nullptr,
                                                    reinterpret_cast<i64*>(labels_dev)); });
   launch(c, K_CLEAR, [&] { k_clear<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e]); });
   launch(c, K_CLEAR, [&] { k_reset_count<<<1, 1, 0, c->st>>>(&ctrl->k[e]); });
@@ -426,10 +446,9 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
 }
 
 // One-time counting sort of the iterate by initial cell (see k_scatter).
-// Leaves table buffer 0 clean; y[0] holds the sorted iterate afterwards and
-// the returned perm maps sorted position -> original point index.
+// Leaves table buffer 0 clean; y[0] holds the sorted iterate afterwards.
 template <int D, class Tab>
-const u32* spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
+SortInfo spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   // dense: scan every slot in key order (lexicographic cell order);
@@ -437,20 +456,35 @@ const u32* spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   const u64 nitems = Tab::kDense ? p.slots : p.list_cap;
   const int nbs = (int)((nitems + kScanChunk - 1) / kScanChunk);
   u64* bsum = ensure<u64>(c, c->scan, (size_t)nbs + 1);
-  u32* off = ensure<u32>(c, c->aux, p.slots);
-  u32* perm = ensure<u32>(c, c->perm, (size_t)n);
+  SortInfo si;
+  u32* off = ensure<u32>(c, c->runoff, p.slots);
+  si.start = ensure<u32>(c, c->runstart, p.slots);
+  si.minidx = ensure<u32>(c, c->runmin, p.slots);
+  si.runs = ensure<u32>(c, c->runlist, p.list_cap);
+  si.cell0 = ensure<u32>(c, c->cell0, (size_t)n);
+  si.runroot = off;   // the cursors are dead once the scatter is done
+  GS_CUDA(cudaMemsetAsync(si.minidx, 0xff, p.slots * sizeof(u32), c->st));
   double* y0 = static_cast<double*>(c->y[0].p);
   double* y1 = static_cast<double*>(c->y[1].p);
   const u32* list = Tab::kDense ? nullptr : tabs[0].list;
   launch(c, K_SORT, [&] { k_hist<D, Tab, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
+  if constexpr (Tab::kDense) {
+    launch(c, K_SORT, [&] {
+      k_compact<D><<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(tabs[0].ent, p.slots, si.runs, &ctrl->nruns);
+    });
+  } else {
+    GS_CUDA(cudaMemcpyAsync(si.runs, tabs[0].list, p.list_cap * sizeof(u32), cudaMemcpyDeviceToDevice, c->st));
+    GS_CUDA(cudaMemcpyAsync(&ctrl->nruns, &ctrl->k[0], sizeof(u32), cudaMemcpyDeviceToDevice, c->st));
+  }
   launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, p.slots); });
   launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
-  launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, off, p.slots); });
-  launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, y1, n, p.g, tabs[0], off, perm, ctrl); });
+  launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, off, p.slots, si.start); });
+  launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, y1, n, p.g, tabs[0], off, nullptr,
+                                                                            si.cell0, si.minidx, ctrl); });
   clear_table<D>(c, p, tabs[0], &ctrl->k[0]);
   check_launch();
   std::swap(c->y[0], c->y[1]);
-  return perm;
+  return si;
 }
 
 struct RunOut {
@@ -478,9 +512,10 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   GS_CUDA(cudaMemsetAsync(fp, 0, sizeof(u64) * max_iters, c->st));
   GS_CUDA(cudaMemsetAsync(c->k_hist.p, 0, sizeof(u32) * max_iters, c->st));
   reset_ctrl(c);
-  const u32* perm = nullptr;
-  if (n >= kSortMinPoints)
-    perm = p.dense ? spatial_sort<D>(c, p, tabs.dn, n) : spatial_sort<D>(c, p, tabs.hs, n);
+  SortInfo sinfo;
+  const bool sorted = n >= kSortMinPoints;
+  if (sorted)
+    sinfo = p.dense ? spatial_sort<D>(c, p, tabs.dn, n) : spatial_sort<D>(c, p, tabs.hs, n);
   if (p.dense)
     enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
   else
@@ -506,10 +541,11 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   r.converged = c->h_ctrl->done;
   const int e = r.iters & 1;
   const double* yf = static_cast<const double*>(c->y[e].p);
+  const SortInfo* sp = (sorted && r.iters >= 1) ? &sinfo : nullptr;
   if (p.dense)
-    run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev, perm, true);
+    run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev, sp, true);
   else
-    run_extract<D>(c, p, tabs.hs, yf, n, e, labels_dev, perm, true);
+    run_extract<D>(c, p, tabs.hs, yf, n, e, labels_dev, sp, true);
   r.k = c->k_last;
   if (movement_out)
     GS_CUDA(cudaMemcpyAsync(movement_out, c->mv_hist.p, sizeof(double) * r.iters, cudaMemcpyDeviceToHost, c->st));
@@ -743,7 +779,8 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->list[0], &c->list[1], &c->targets, &c->partials, &c->par, &c->first, &c->aux,
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
-                 &c->track_out, &c->bitmaps, &c->scan};
+                 &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
+                 &c->runlist, &c->cell0};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);

@@ -880,7 +880,7 @@ __global__ void __launch_bounds__(1024) k_scan_top(u64* bsum, int nb) {
 // per-cell write cursor = exclusive prefix of counts (list order)
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, const u32* list, const u32* kp,
-                                                         const u64* bsum, u32* off, u64 nslots) {
+                                                         const u64* bsum, u32* off, u64 nslots, u32* start) {
   const u64 k = list ? (u64)*kp : nslots;
   const i64 a0 = (i64)blockIdx.x * kScanChunk;
   if (a0 >= (i64)k) return;
@@ -904,15 +904,21 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, co
   for (int q = 0; q < (int)(threadIdx.x >> 5); ++q) pre += w[q];
   for (int it = 0; it < kScanItems; ++it) {
     const i64 a = a0 + (i64)threadIdx.x * kScanItems + it;
-    if (a < (i64)k) off[scan_item(list, a)] = (u32)pre;
+    if (a < (i64)k) {
+      off[scan_item(list, a)] = (u32)pre;
+      if (start) start[scan_item(list, a)] = (u32)pre;
+    }
     pre += c[it];
   }
 }
 
-// scatter points into cell order; warp-aggregated cursor bumps
+// scatter points into cell order; warp-aggregated cursor bumps.  Also
+// records, for the run-based extraction, each point's initial cell slot in
+// ORIGINAL order (coalesced) and each run's minimum original index.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__ y, double* __restrict__ ys, i64 n,
-                                                      GridParams g, Tab tab, u32* off, u32* perm, Ctrl* ctrl) {
+                                                      GridParams g, Tab tab, u32* off, u32* perm, u32* cell0,
+                                                      u32* minidx, Ctrl* ctrl) {
   const int lane = threadIdx.x & 31;
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
@@ -926,19 +932,60 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__
       bool inside;
       const u64 key = pack_key<D>(g, v, inside);
       if (!inside || !tab.find(key, s)) { atomicOr(&ctrl->error, kErrMissing); s = 0xffffffffu; }
+      cell0[i] = s;
     }
     const unsigned peers = __match_any_sync(kFull, s);
     const int leader = __ffs(peers) - 1;
+    const u32 mi = __reduce_min_sync(peers, (u32)i);
     u32 basepos = 0;
-    if (lane == leader && s != 0xffffffffu) basepos = atomicAdd(off + s, (u32)__popc(peers));
+    if (lane == leader && s != 0xffffffffu) {
+      basepos = atomicAdd(off + s, (u32)__popc(peers));
+      atomicMin(minidx + s, mi);
+    }
     basepos = __shfl_sync(kFull, basepos, leader);
     if (s != 0xffffffffu) {
       const u32 pos = basepos + __popc(peers & ((1u << lane) - 1u));
 #pragma unroll
       for (int j = 0; j < D; ++j) ys[(i64)j * g.ld + pos] = v[j];
-      perm[pos] = (u32)i;
+      if (perm) perm[pos] = (u32)i;
     }
   }
+}
+
+// Run-based extraction (after the spatial sort, at least one iteration).
+// A run = the points of one initial cell: contiguous in sorted order and,
+// from iteration 1 on, bitwise-identical positions.  Per run: its final
+// cell's component root (stored over the run's cursor slot) and the
+// first-appearance minimum over its original indices (modeseek.py:262-265).
+template <int D, class Tab>
+__global__ void k_run_first(const double* __restrict__ yf, GridParams g, Tab tab, const u32* runs,
+                            const u32* nruns, const u32* start, const u32* minidx, const u32* par,
+                            u32* first, u32* runroot, Ctrl* ctrl) {
+  const u32 R = *nruns;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < R; a += stride) {
+    const u32 s0 = runs[a];
+    const u32 p = start[s0];
+    double v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = yf[(i64)j * g.ld + p];
+    bool inside;
+    const u64 key = pack_key<D>(g, v, inside);
+    u32 sf = 0;
+    if (!inside || !tab.find(key, sf)) { atomicOr(&ctrl->error, kErrMissing); continue; }
+    const u32 r = par[sf];
+    runroot[s0] = r;
+    atomicMin(first + r, minidx[s0]);
+  }
+}
+
+// labels in original order: one coalesced pass (cell0 -> run root -> rank)
+__global__ void __launch_bounds__(kThreads) k_labels_runs(const u32* __restrict__ cell0, i64 n,
+                                                          const u32* __restrict__ runroot,
+                                                          const u32* __restrict__ rankmap, i64* labels) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    labels[i] = (i64)rankmap[runroot[cell0[i]]];
 }
 
 // ------------------------------------------------------------- extraction
