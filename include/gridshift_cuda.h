@@ -20,8 +20,9 @@
  *
  * Host-pointer entry points copy inputs host->device and results
  * device->host inside the call (pinned host buffers make those copies
- * full-speed).  The *_device variants take device pointers and a
- * cudaStream_t (as void*) and leave results on the device.
+ * full-speed).  The *_device / gs_shard_* variants take device pointers and
+ * a cudaStream_t (as void*, NULL = legacy default stream) and leave results
+ * on the device.
  */
 #ifndef GRIDSHIFT_CUDA_H
 #define GRIDSHIFT_CUDA_H
@@ -85,8 +86,9 @@ GS_API int gs_meanshiftpp(gs_ctx* ctx, const double* x, int64_t n, int32_t d, do
 /* Same engine on device-resident input (x_dev: (n,d) row-major, dtype
  * GS_DTYPE_F64 or GS_DTYPE_F32 -- f32 is upcast on device as PointSet
  * does on the host, grid.py:43).  labels_dev: (n,) int64 device buffer.
- * stream: cudaStream_t or NULL for the context's own stream.  Returns after
- * the stream work completed. */
+ * stream: the cudaStream_t to run on, taken literally (NULL = the legacy
+ * default stream, e.g. torch's default stream).  Returns after the stream
+ * work completed. */
 GS_API int gs_meanshiftpp_device(gs_ctx* ctx, const void* x_dev, int32_t dtype, int64_t n, int32_t d,
                           double h, double eta, int32_t max_iters, int64_t* labels_dev,
                           int64_t* k_out, int32_t* iters_out, double* movement_out,
@@ -157,6 +159,41 @@ GS_API int gs_track_sequence(gs_ctx* ctx, const uint8_t* frames, int32_t n_frame
 /* Bin set B after the last gs_track_sequence frame (two-phase like
  * gs_build_tables). */
 GS_API int gs_fetch_track_bins(gs_ctx* ctx, int64_t* bins_out, int32_t cap, int32_t* nb_out);
+
+/*
+ * Row-sharded run (one process per GPU; cfg4-style strong scaling).  The
+ * caller owns the collectives (e.g. NCCL through torch.distributed) and
+ * drives:
+ *   gs_shard_init        local input -> per-axis cell range / max|x| / flags
+ *   (all-reduce MIN cmin, MAX cmax, MAX absmax, OR flags)
+ *   gs_shard_plan        global plan; local spatial sort; local first table
+ *   gs_shard_table_io    export (0) / import (1) the table words (int64)
+ *   (all-reduce SUM of the table words: exact integer merge)
+ *   per iteration t:     gs_shard_iterate -> (all-reduce SUM of 4 int64
+ *                        limbs) -> gs_shard_converge; gs_shard_status between
+ *                        chunks
+ *   gs_shard_components  local first-appearance minima per component root
+ *   (all-reduce MIN of the int64 minima, slots entries)
+ *   gs_shard_finish      labels of the local rows (global first-appearance
+ *                        numbering), k, trace; modes via gs_fetch_modes.
+ * Every rank derives identical tables, so no per-iteration table exchange is
+ * needed.  Same reference semantics as gs_meanshiftpp (modeseek.py:125-146).
+ */
+GS_API int gs_shard_init(gs_ctx* ctx, const void* x_dev, int32_t dtype, int64_t n_local, int32_t d,
+                         double h, void* stream, int64_t* cmin_out, int64_t* cmax_out,
+                         double* absmax_out, int32_t* flags_out);
+GS_API int gs_shard_plan(gs_ctx* ctx, const int64_t* cmin, const int64_t* cmax, const double* absmax,
+                         int32_t flags, int64_t n_total, int32_t max_iters, void* stream,
+                         int64_t* table_words_out);
+GS_API int gs_shard_table_io(gs_ctx* ctx, void* buf_dev, int32_t to_device_table, void* stream);
+GS_API int gs_shard_iterate(gs_ctx* ctx, int32_t t, void* limbs_dev, void* stream);
+GS_API int gs_shard_converge(gs_ctx* ctx, int32_t t, const void* limbs_dev, double eta, void* stream);
+GS_API int gs_shard_status(gs_ctx* ctx, int32_t* done_out, int32_t* iters_out, void* stream);
+GS_API int gs_shard_components(gs_ctx* ctx, int64_t global_offset, void* minima_dev, void* stream,
+                               int64_t* slots_out);
+GS_API int gs_shard_finish(gs_ctx* ctx, const void* minima_dev, int64_t* labels_dev, void* stream,
+                           int64_t* k_out, int32_t* iters_out, double* movement_out,
+                           int32_t* converged_out);
 
 #ifdef __cplusplus
 }

@@ -46,6 +46,14 @@ SIGNATURES = {
     "gs_track_sequence": (C.c_int, [_P, _P, _i32, _i32, _i32, _f64, _f64, _i32, _i32, _P, _i32,
                                     _f64, _i32, _i32, _f64, _i32, _P, _P, _P, _P, _P, _P]),
     "gs_fetch_track_bins": (C.c_int, [_P, _P, _i32, _P]),
+    "gs_shard_init": (C.c_int, [_P, _P, _i32, _i64, _i32, _f64, _P, _P, _P, _P, _P]),
+    "gs_shard_plan": (C.c_int, [_P, _P, _P, _P, _i32, _i64, _i32, _P, _P]),
+    "gs_shard_table_io": (C.c_int, [_P, _P, _i32, _P]),
+    "gs_shard_iterate": (C.c_int, [_P, _i32, _P, _P]),
+    "gs_shard_converge": (C.c_int, [_P, _i32, _P, _f64, _P]),
+    "gs_shard_status": (C.c_int, [_P, _P, _P, _P]),
+    "gs_shard_components": (C.c_int, [_P, _i64, _P, _P, _P]),
+    "gs_shard_finish": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

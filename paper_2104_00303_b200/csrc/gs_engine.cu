@@ -90,6 +90,7 @@ struct gs_ctx {
   std::vector<uint64_t> iter_fp;
   std::vector<int64_t> track_bins;
   Prof prof;
+  struct ShardState* shard = nullptr;   // row-sharded run in progress (gs_shard_*)
 };
 
 namespace {
@@ -333,7 +334,7 @@ void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_p
 // the table of y_{t+1} from it (O(cells)), k_shift moves every point.
 template <int D, class Tab>
 void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, int64_t n, int nb_pts,
-                       int nb_cells) {
+                       int nb_cells, u64* limbs = nullptr) {
   const int cur = t & 1;
   double* y_in = static_cast<double*>(c->y[cur].p);
   double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
@@ -346,7 +347,7 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
                                                                                 ctrl, cur); });
   launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec, ctrl,
                                                   static_cast<u64*>(c->partials.p),
-                                                  static_cast<double*>(c->mv_hist.p), t, eta); });
+                                                  static_cast<double*>(c->mv_hist.p), t, eta, limbs); });
 }
 
 // Occupied-cell list of a table (hash tables maintain theirs on insert;
@@ -375,9 +376,11 @@ void clear_table(gs_ctx* c, const Plan& p, Tab& tab, u32* kp) {
 // entry, buffer e^1 is dirty (cleared here and used as component scratch).
 // `table_ready`: buffer e already holds the table of yf (the last k_step
 // built it); otherwise it is clean and gets built here.
+// Phase 1: components of the final table + this process's first-appearance
+// minima (`offset` = global index of its first point, sharded runs).
 template <int D, class Tab>
-void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
-                 int64_t* labels_dev, const SortInfo* si = nullptr, bool table_ready = false) {
+void extract_components(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
+                        const SortInfo* si, bool table_ready, u32 offset) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
@@ -390,20 +393,34 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
   }
   u32* par = ensure<u32>(c, c->par, p.slots);
   u32* first = ensure<u32>(c, c->first, p.slots);
-  u32* rankmap = ensure<u32>(c, c->aux, p.slots);
-  u32* roots = ensure<u32>(c, c->roots, p.list_cap + 1);
-  u32* rfirst = ensure<u32>(c, c->root_first, p.list_cap + 1);
-  u32* nroots = ensure<u32>(c, c->partials, 2 * (size_t)c->sms * 8 + 2);  // reuse scratch
   launch(c, K_COMP, [&] { k_uf_init<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first); });
   launch(c, K_COMP, [&] { k_uf_link<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[e], &ctrl->k[e], par); });
   launch(c, K_COMP, [&] { k_uf_flatten<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, tabs[e ^ 1].ent); });
   if (si)
     launch(c, K_LABELS, [&] {
       k_run_first<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(yf, p.g, tabs[e], si->runs, &ctrl->nruns, si->start,
-                                                            si->minidx, par, first, si->runroot, ctrl);
+                                                            si->minidx, par, first, si->runroot, ctrl, offset);
     });
   else
-    launch(c, K_LABELS, [&] { k_first<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, first, nullptr, ctrl); });
+    launch(c, K_LABELS, [&] {
+      k_first<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(yf, n, p.g, tabs[e], par, first, nullptr, ctrl, offset);
+    });
+}
+
+// Phase 2: dense relabel by first appearance, modes, labels; leaves both
+// table buffers clean.
+template <int D, class Tab>
+void extract_finish(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
+                    int64_t* labels_dev, const SortInfo* si) {
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  const int nb_pts = blocks_for(c, n);
+  const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
+  u32* par = static_cast<u32*>(c->par.p);
+  u32* first = static_cast<u32*>(c->first.p);
+  u32* rankmap = ensure<u32>(c, c->aux, p.slots);
+  u32* roots = ensure<u32>(c, c->roots, p.list_cap + 1);
+  u32* rfirst = ensure<u32>(c, c->root_first, p.list_cap + 1);
+  u32* nroots = ensure<u32>(c, c->partials, 2 * (size_t)c->sms * 8 + 2);  // reuse scratch
   GS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(u32), c->st));
   launch(c, K_COMP, [&] { k_roots<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first, roots, rfirst, nroots); });
   check_launch();
@@ -443,6 +460,13 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
   sync(c);
   c->k_last = nr;
   c->d_last = D;
+}
+
+template <int D, class Tab>
+void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t n, int e,
+                 int64_t* labels_dev, const SortInfo* si = nullptr, bool table_ready = false) {
+  extract_components<D>(c, p, tabs, yf, n, e, si, table_ready, 0u);
+  extract_finish<D>(c, p, tabs, yf, n, e, labels_dev, si);
 }
 
 // One-time counting sort of the iterate by initial cell (see k_scatter).
@@ -739,6 +763,104 @@ double* stage_input(gs_ctx* c, const double* x, int64_t n, int d) {
 
 }  // namespace
 
+// ------------------------------------------------------------- sharded runs
+// A row shard of one MeanShift++ run (one process per GPU).  Only the first
+// cell table is merged across ranks (integer all-reduce: exact, identical on
+// every rank); every later table is derived from the global one (k_derive)
+// on every rank alike, so an iteration exchanges just the 4-limb movement.
+
+struct ShardState {
+  int d = 0;
+  int64_t n = 0;
+  int64_t n_total = 0;
+  double h = 0;
+  int max_iters = 0;
+  Plan p{};
+  SortInfo si{};
+  bool sorted = false;
+};
+
+ShardState* shard_of(gs_ctx* c, bool create) {
+  if (!c->shard) {
+    if (!create) fail(GS_EINVAL, "no sharded run in progress on this context");
+    c->shard = new ShardState();
+  }
+  return c->shard;
+}
+
+template <int D>
+void shard_plan_d(gs_ctx* c, ShardState* sh, const InitStats& s) {
+  Plan p = make_plan(sh->n_total, D, sh->h, s);
+  if (!p.dense) fail(GS_EUNSUPPORTED, "row sharding needs a dense lattice table (shard by image instead)");
+  p.g.ld = soa_ld(sh->n);
+  sh->p = p;
+  Tabs<D> tabs = make_tabs<D>(c, p);
+  ensure<Rec<D>>(c, c->targets, p.slots);
+  const int nb_pts = blocks_for(c, sh->n);
+  ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
+  ensure<double>(c, c->mv_hist, (size_t)sh->max_iters);
+  GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->fp_hist, (size_t)sh->max_iters), 0, 8 * sh->max_iters, c->st));
+  GS_CUDA(cudaMemsetAsync(ensure<u32>(c, c->k_hist, (size_t)sh->max_iters), 0, 4 * sh->max_iters, c->st));
+  reset_ctrl(c);
+  sh->sorted = sh->n >= kSortMinPoints;
+  if (sh->sorted) sh->si = spatial_sort<D>(c, p, tabs.dn, sh->n);
+  enqueue_first_hist<D>(c, p, tabs.dn, sh->n, nb_pts);
+  check_launch();
+}
+
+template <int D>
+void shard_iterate_d(gs_ctx* c, ShardState* sh, int t, u64* limbs) {
+  Tabs<D> tabs = make_tabs<D>(c, sh->p);
+  enqueue_iteration<D>(c, sh->p, tabs.dn, t, 0.0, sh->n, blocks_for(c, sh->n),
+                       blocks_for(c, (int64_t)sh->p.list_cap), limbs);
+  check_launch();
+}
+
+template <int D>
+void shard_components_d(gs_ctx* c, ShardState* sh, u32 offset, long long* minima) {
+  Tabs<D> tabs = make_tabs<D>(c, sh->p);
+  read_ctrl(c);
+  check_flags(c->h_ctrl->error);
+  const int e = c->h_ctrl->iters & 1;
+  const double* yf = static_cast<const double*>(c->y[e].p);
+  const SortInfo* sp = (sh->sorted && c->h_ctrl->iters >= 1) ? &sh->si : nullptr;
+  extract_components<D>(c, sh->p, tabs.dn, yf, sh->n, e, sp, true, offset);
+  GS_CUDA(cudaMemsetAsync(minima, 0x7f, sh->p.slots * sizeof(long long), c->st));
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  launch(c, K_COMP, [&] {
+    k_export_minima<D, DenseTable<D>><<<blocks_for(c, (int64_t)sh->p.list_cap), kThreads, 0, c->st>>>(
+        tabs.dn[e], &ctrl->k[e], static_cast<u32*>(c->par.p), static_cast<u32*>(c->first.p), minima);
+  });
+  check_launch();
+}
+
+template <int D>
+void shard_finish_d(gs_ctx* c, ShardState* sh, const long long* minima, int64_t* labels_dev) {
+  Tabs<D> tabs = make_tabs<D>(c, sh->p);
+  const int e = c->h_ctrl->iters & 1;
+  const double* yf = static_cast<const double*>(c->y[e].p);
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  launch(c, K_COMP, [&] {
+    k_import_minima<D, DenseTable<D>><<<blocks_for(c, (int64_t)sh->p.list_cap), kThreads, 0, c->st>>>(
+        tabs.dn[e], &ctrl->k[e], static_cast<u32*>(c->par.p), static_cast<u32*>(c->first.p), minima);
+  });
+  const SortInfo* sp = (sh->sorted && c->h_ctrl->iters >= 1) ? &sh->si : nullptr;
+  extract_finish<D>(c, sh->p, tabs.dn, yf, sh->n, e, labels_dev, sp);
+}
+
+#define GS_DISPATCH(d, CALL)                                                    \
+  switch (d) {                                                                  \
+    case 1: { constexpr int DD = 1; CALL; } break;                               \
+    case 2: { constexpr int DD = 2; CALL; } break;                               \
+    case 3: { constexpr int DD = 3; CALL; } break;                               \
+    case 4: { constexpr int DD = 4; CALL; } break;                               \
+    case 5: { constexpr int DD = 5; CALL; } break;                               \
+    case 6: { constexpr int DD = 6; CALL; } break;                               \
+    case 7: { constexpr int DD = 7; CALL; } break;                               \
+    case 8: { constexpr int DD = 8; CALL; } break;                               \
+    default: fail(GS_EUNSUPPORTED, "unsupported d");                              \
+  }
+
 // ===================================================================== C ABI
 
 extern "C" {
@@ -787,6 +909,7 @@ void gs_ctx_destroy(gs_ctx* c) {
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->h_small) cudaFreeHost(c->h_small);
   for (cudaEvent_t e : c->prof.pool) cudaEventDestroy(e);
+  delete c->shard;
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -816,7 +939,7 @@ int gs_meanshiftpp_device(gs_ctx* c, const void* x_dev, int32_t dtype, int64_t n
     validate_run(n, d, h, eta, max_iters);
     if (!x_dev || !labels_dev) fail(GS_EINVAL, "null buffer");
     if (dtype != GS_DTYPE_F64 && dtype != GS_DTYPE_F32) fail(GS_EINVAL, "dtype must be f64 or f32");
-    if (stream) c->st = static_cast<cudaStream_t>(stream);
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
     Input in{dtype == GS_DTYPE_F64 ? IN_F64 : IN_F32, x_dev};
     RunOut r = run_engine(c, in, n, d, h, eta, max_iters, labels_dev, movement_out);
     sync(c);
@@ -1042,6 +1165,132 @@ int gs_fetch_track_bins(gs_ctx* c, int64_t* bins_out, int32_t cap, int32_t* nb_o
     const int32_t nb = (int32_t)(c->track_bins.size() / 3);
     if (nb_out) *nb_out = nb;
     if (bins_out && cap >= nb) memcpy(bins_out, c->track_bins.data(), c->track_bins.size() * 8);
+  });
+}
+
+int gs_shard_init(gs_ctx* c, const void* x_dev, int32_t dtype, int64_t n_local, int32_t d, double h,
+                  void* stream, int64_t* cmin_out, int64_t* cmax_out, double* absmax_out, int32_t* flags_out) {
+  return guarded(c, [&] {
+    validate_common(n_local, d, h);
+    if (!x_dev) fail(GS_EINVAL, "null buffer");
+    if (dtype != GS_DTYPE_F64 && dtype != GS_DTYPE_F32) fail(GS_EINVAL, "dtype must be f64 or f32");
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    ShardState* sh = shard_of(c, true);
+    sh->d = d;
+    sh->n = n_local;
+    sh->h = h;
+    Input in{dtype == GS_DTYPE_F64 ? IN_F64 : IN_F32, x_dev};
+    InitStats st{};
+    GS_DISPATCH(d, {
+      double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n_local) * DD);
+      ensure<double>(c, c->y[1], (size_t)soa_ld(n_local) * DD);
+      ensure<Ctrl>(c, c->ctrl, 1);
+      st = run_init<DD>(c, in, n_local, h, y0);
+    });
+    for (int j = 0; j < d; ++j) {
+      cmin_out[j] = st.cmin[j];
+      cmax_out[j] = st.cmax[j];
+      memcpy(&absmax_out[j], &st.absmax[j], 8);
+    }
+    *flags_out = st.flags;
+  });
+}
+
+int gs_shard_plan(gs_ctx* c, const int64_t* cmin, const int64_t* cmax, const double* absmax, int32_t flags,
+                  int64_t n_total, int32_t max_iters, void* stream, int64_t* table_words_out) {
+  return guarded(c, [&] {
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    ShardState* sh = shard_of(c, false);
+    if (max_iters < 1) fail(GS_EINVAL, "max_iters must be a positive integer");
+    if (n_total < sh->n || n_total >= (int64_t)UINT32_MAX) fail(GS_EINVAL, "bad n_total");
+    sh->n_total = n_total;
+    sh->max_iters = max_iters;
+    InitStats s{};
+    for (int j = 0; j < sh->d; ++j) {
+      s.cmin[j] = cmin[j];
+      s.cmax[j] = cmax[j];
+      memcpy(&s.absmax[j], &absmax[j], 8);
+    }
+    s.flags = flags;
+    GS_DISPATCH(sh->d, shard_plan_d<DD>(c, sh, s));
+    *table_words_out = (int64_t)sh->p.slots * (1 + 2 * sh->d);
+  });
+}
+
+int gs_shard_table_io(gs_ctx* c, void* buf_dev, int32_t to_device_table, void* stream) {
+  return guarded(c, [&] {
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    ShardState* sh = shard_of(c, false);
+    const size_t bytes = sh->p.slots * 8 * (1 + 2 * (size_t)sh->d);
+    if (to_device_table)
+      GS_CUDA(cudaMemcpyAsync(c->ent[0].p, buf_dev, bytes, cudaMemcpyDeviceToDevice, c->st));
+    else
+      GS_CUDA(cudaMemcpyAsync(buf_dev, c->ent[0].p, bytes, cudaMemcpyDeviceToDevice, c->st));
+  });
+}
+
+int gs_shard_iterate(gs_ctx* c, int32_t t, void* limbs_dev, void* stream) {
+  return guarded(c, [&] {
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    ShardState* sh = shard_of(c, false);
+    if (t < 0 || t >= sh->max_iters) fail(GS_EINVAL, "iteration out of range");
+    GS_DISPATCH(sh->d, shard_iterate_d<DD>(c, sh, t, static_cast<u64*>(limbs_dev)));
+  });
+}
+
+int gs_shard_converge(gs_ctx* c, int32_t t, const void* limbs_dev, double eta, void* stream) {
+  return guarded(c, [&] {
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    ShardState* sh = shard_of(c, false);
+    launch(c, K_SHIFT, [&] {
+      k_converge<<<1, 1, 0, c->st>>>(static_cast<const u64*>(limbs_dev), sh->p.g, static_cast<Ctrl*>(c->ctrl.p),
+                                     static_cast<double*>(c->mv_hist.p), t, eta);
+    });
+    check_launch();
+  });
+}
+
+int gs_shard_status(gs_ctx* c, int32_t* done_out, int32_t* iters_out, void* stream) {
+  return guarded(c, [&] {
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    shard_of(c, false);
+    read_ctrl(c);
+    check_flags(c->h_ctrl->error);
+    *done_out = c->h_ctrl->done;
+    *iters_out = c->h_ctrl->iters;
+  });
+}
+
+int gs_shard_components(gs_ctx* c, int64_t global_offset, void* minima_dev, void* stream, int64_t* slots_out) {
+  return guarded(c, [&] {
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    ShardState* sh = shard_of(c, false);
+    GS_DISPATCH(sh->d, shard_components_d<DD>(c, sh, (u32)global_offset, static_cast<long long*>(minima_dev)));
+    *slots_out = (int64_t)sh->p.slots;
+  });
+}
+
+int gs_shard_finish(gs_ctx* c, const void* minima_dev, int64_t* labels_dev, void* stream, int64_t* k_out,
+                    int32_t* iters_out, double* movement_out, int32_t* converged_out) {
+  return guarded(c, [&] {
+    c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+    ShardState* sh = shard_of(c, false);
+    GS_DISPATCH(sh->d, shard_finish_d<DD>(c, sh, static_cast<const long long*>(minima_dev), labels_dev));
+    const int iters = c->h_ctrl->iters;
+    if (movement_out)
+      GS_CUDA(cudaMemcpyAsync(movement_out, c->mv_hist.p, sizeof(double) * iters, cudaMemcpyDeviceToHost, c->st));
+    c->iter_k.assign(iters, 0);
+    c->iter_fp.assign(iters, 0);
+    std::vector<u32> kk(iters + 1);
+    GS_CUDA(cudaMemcpyAsync(kk.data(), c->k_hist.p, sizeof(u32) * iters, cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaMemcpyAsync(c->iter_fp.data(), c->fp_hist.p, sizeof(u64) * iters, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    for (int i = 0; i < iters; ++i) c->iter_k[i] = kk[i];
+    *k_out = c->k_last;
+    *iters_out = iters;
+    *converged_out = c->h_ctrl->done;
+    delete c->shard;
+    c->shard = nullptr;
   });
 }
 

@@ -530,7 +530,7 @@ template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads, 3) k_shift(const double* __restrict__ y, double* __restrict__ yo, i64 n,
                                                        GridParams g, Tab tab, const Rec<D>* __restrict__ rec,
                                                        Ctrl* ctrl, u64* partials, double* mv_hist, int t,
-                                                       double eta) {
+                                                       double eta, u64* limbs) {
   if (*(volatile int*)&ctrl->done) return;
   u64 ahi = 0, alo = 0;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -623,11 +623,52 @@ __global__ void __launch_bounds__(kThreads, 3) k_shift(const double* __restrict_
   if (threadIdx.x == 0) {
     u64 bh = 0, bl = 0;
     for (int qq = 0; qq < (int)(blockDim.x >> 5); ++qq) add128(bh, bl, sh[qq][0], sh[qq][1]);
+    ctrl->blocks_done = 0;
+    if (limbs) {
+      // sharded run: this rank's exact total as 32-bit limbs, summed across
+      // ranks by an integer all-reduce, then k_converge
+      limbs[0] = bl & 0xffffffffull;
+      limbs[1] = bl >> 32;
+      limbs[2] = bh & 0xffffffffull;
+      limbs[3] = bh >> 32;
+      return;
+    }
     const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
     mv_hist[t] = mv;
     ctrl->iters = t + 1;
-    ctrl->blocks_done = 0;
     if (mv < eta) ctrl->done = 1;
+  }
+}
+
+// Sharded run: global movement from the all-reduced limbs (exact).
+__global__ void k_converge(const u64* limbs, GridParams g, Ctrl* ctrl, double* mv_hist, int t, double eta) {
+  if (*(volatile int*)&ctrl->done) return;
+  const u128 tot = (u128)limbs[0] + ((u128)limbs[1] << 32) + ((u128)limbs[2] << 64) + ((u128)limbs[3] << 96);
+  const double mv = u128_to_double(tot, g.movement_exp - 96);
+  mv_hist[t] = mv;
+  ctrl->iters = t + 1;
+  if (mv < eta) ctrl->done = 1;
+}
+
+// Sharded run: per-root first-appearance minima (global indices) for a MIN
+// all-reduce; non-roots stay at the sentinel.
+template <int D, class Tab>
+__global__ void k_export_minima(Tab tab, const u32* kp, const u32* par, const u32* first, long long* minima) {
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    if (par[s] == s && first[s] != 0xffffffffu) minima[s] = (long long)first[s];
+  }
+}
+
+template <int D, class Tab>
+__global__ void k_import_minima(Tab tab, const u32* kp, const u32* par, u32* first, const long long* minima) {
+  const u32 k = *kp;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
+    const u32 s = tab.list[a];
+    if (par[s] == s) first[s] = (u32)minima[s];
   }
 }
 
@@ -960,7 +1001,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__
 template <int D, class Tab>
 __global__ void k_run_first(const double* __restrict__ yf, GridParams g, Tab tab, const u32* runs,
                             const u32* nruns, const u32* start, const u32* minidx, const u32* par,
-                            u32* first, u32* runroot, Ctrl* ctrl) {
+                            u32* first, u32* runroot, Ctrl* ctrl, u32 offset) {
   const u32 R = *nruns;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < R; a += stride) {
@@ -975,7 +1016,7 @@ __global__ void k_run_first(const double* __restrict__ yf, GridParams g, Tab tab
     if (!inside || !tab.find(key, sf)) { atomicOr(&ctrl->error, kErrMissing); continue; }
     const u32 r = par[sf];
     runroot[s0] = r;
-    atomicMin(first + r, minidx[s0]);
+    atomicMin(first + r, minidx[s0] + offset);
   }
 }
 
@@ -1089,7 +1130,8 @@ __global__ void k_uf_flatten(Tab tab, const u32* kp, u32* par, Entry<D>* acc) {
 // with match_any + reduce_min before the single atomicMin.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_first(const double* __restrict__ y, i64 n, GridParams g, Tab tab,
-                                                    const u32* par, u32* first, const u32* perm, Ctrl* ctrl) {
+                                                    const u32* par, u32* first, const u32* perm, Ctrl* ctrl,
+                                                    u32 offset) {
   const int lane = threadIdx.x & 31;
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
@@ -1105,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads) k_first(const double* __restrict__ y
       u32 s;
       if (inside && tab.find(key, s)) {
         r = par[s];
-        idx = perm ? perm[i] : (u32)i;
+        idx = (perm ? perm[i] : (u32)i) + offset;
       } else {
         atomicOr(&ctrl->error, kErrMissing);
       }
