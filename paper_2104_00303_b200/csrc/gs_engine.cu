@@ -77,7 +77,7 @@ struct gs_ctx {
   // device buffers
   Buf x_stage, y[2], ent[2], keys[2], list[2], targets, partials, par, first, aux, roots,
       root_first, ranks, modes, labels, mv_hist, fp_hist, k_hist, stats, ctrl, perm, track,
-      track_out, bitmaps, scan, runoff, runstart, runmin, runlist, cell0;
+      track_out, bitmaps, scan, runoff, runstart, runmin, runlist, cell0, stage;
   // pinned host mirrors
   Ctrl* h_ctrl = nullptr;
   InitStats* h_stats = nullptr;
@@ -503,8 +503,10 @@ SortInfo spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, p.slots); });
   launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
   launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, off, p.slots, si.start); });
-  launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, y1, n, p.g, tabs[0], off, nullptr,
+  double* stage = ensure<double>(c, c->stage, (size_t)n * StageRec<D>::W);
+  launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, stage, n, p.g, tabs[0], off, nullptr,
                                                                             si.cell0, si.minidx, ctrl); });
+  launch(c, K_SORT, [&] { k_unstage<D><<<nb_pts, kThreads, 0, c->st>>>(stage, y1, n, p.g.ld); });
   clear_table<D>(c, p, tabs[0], &ctrl->k[0]);
   check_launch();
   std::swap(c->y[0], c->y[1]);
@@ -902,7 +904,7 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
                  &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
-                 &c->runlist, &c->cell0};
+                 &c->runlist, &c->cell0, &c->stage};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);

@@ -956,8 +956,16 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, co
 // scatter points into cell order; warp-aggregated cursor bumps.  Also
 // records, for the run-based extraction, each point's initial cell slot in
 // ORIGINAL order (coalesced) and each run's minimum original index.
+// Scatter target: whole AoS records (D doubles padded to 16-byte multiples),
+// so every random write covers full 32-byte sectors (no partial-sector
+// read-modify-write); k_unstage transposes back to SoA with coalesced I/O.
+template <int D>
+struct StageRec {
+  static constexpr int W = (D + 1) & ~1;   // doubles per record
+};
+
 template <int D, class Tab>
-__global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__ y, double* __restrict__ ys, i64 n,
+__global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__ y, double* __restrict__ stage, i64 n,
                                                       GridParams g, Tab tab, u32* off, u32* perm, u32* cell0,
                                                       u32* minidx, Ctrl* ctrl) {
   const int lane = threadIdx.x & 31;
@@ -986,10 +994,32 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__
     basepos = __shfl_sync(kFull, basepos, leader);
     if (s != 0xffffffffu) {
       const u32 pos = basepos + __popc(peers & ((1u << lane) - 1u));
+      constexpr int W = StageRec<D>::W;
+      double2* dst = reinterpret_cast<double2*>(stage + (i64)pos * W);
 #pragma unroll
-      for (int j = 0; j < D; ++j) ys[(i64)j * g.ld + pos] = v[j];
+      for (int q = 0; q < W / 2; ++q)
+        dst[q] = make_double2(v[2 * q], (2 * q + 1 < D) ? v[2 * q + 1] : 0.0);
       if (perm) perm[pos] = (u32)i;
     }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_unstage(const double* __restrict__ stage, double* __restrict__ ys, i64 n,
+                                                      i64 ld) {
+  constexpr int W = StageRec<D>::W;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double2* src = reinterpret_cast<const double2*>(stage + i * W);
+    double v[W];
+#pragma unroll
+    for (int q = 0; q < W / 2; ++q) {
+      const double2 a = __ldcs(src + q);
+      v[2 * q] = a.x;
+      v[2 * q + 1] = a.y;
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * ld + i, v[j]);
   }
 }
 
