@@ -340,9 +340,29 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
   double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   Rec<D>* rec = static_cast<Rec<D>*>(c->targets.p);
-  launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur,
-                                                  static_cast<u64*>(c->fp_hist.p) + t,
-                                                  static_cast<u32*>(c->k_hist.p) + t); });
+  bool bricked = false;
+  if constexpr (D == 3 && Tab::kDense) {
+    // dense 3-D lattice: tiled stencil (k_agg_brick3)
+    const int ext0 = (int)(p.g.nkeys / p.g.stride[0]), ext1 = (int)(p.g.stride[0] / p.g.stride[1]),
+              ext2 = (int)p.g.stride[1];
+    const int nbx = (ext0 + kBrick - 1) / kBrick, nby = (ext1 + kBrick - 1) / kBrick,
+              nbz = (ext2 + kBrick - 1) / kBrick;
+    static bool attr = false;
+    if (!attr) {
+      GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBrickSmem));
+      attr = true;
+    }
+    launch(c, K_AGG, [&] {
+      k_agg_brick3<<<nbx * nby * nbz, kBrickThreads, kBrickSmem, c->st>>>(
+          p.g, tabs[cur], tabs[cur ^ 1], reinterpret_cast<Rec<3>*>(rec), ctrl,
+          static_cast<u64*>(c->fp_hist.p) + t, static_cast<u32*>(c->k_hist.p) + t, nbx, nby, nbz);
+    });
+    bricked = true;
+  }
+  if (!bricked)
+    launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur,
+                                                    static_cast<u64*>(c->fp_hist.p) + t,
+                                                    static_cast<u32*>(c->k_hist.p) + t); });
   launch(c, K_DERIVE, [&] { k_derive<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
                                                                                 ctrl, cur); });
   launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec, ctrl,

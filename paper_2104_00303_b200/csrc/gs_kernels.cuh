@@ -672,6 +672,104 @@ __global__ void k_import_minima(Tab tab, const u32* kp, const u32* par, u32* fir
   }
 }
 
+// Dense 3-D tables: tiled 3x3x3 stencil.  A block owns an 8x8x8 brick of
+// lattice slots, stages the 10x10x10 halo of table entries in shared memory
+// once (~110 B of global reads per cell instead of 27 scattered entry
+// reads), skips bricks with no occupied cell, and for every occupied cell
+// sums its 27 neighbours from shared memory (exact integer sums), rounds
+// once and divides (grid.py:230-259, modeseek.py:109).  Also clears the
+// previous table inside the brick and records k and the fingerprint.
+constexpr int kBrick = 8;
+constexpr int kHalo = kBrick + 2;
+constexpr int kBrickThreads = 512;
+constexpr size_t kBrickSmem = (size_t)kHalo * kHalo * kHalo * sizeof(Entry<3>);
+
+__global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, DenseTable<3> tab, DenseTable<3> prev,
+                                                              Rec<3>* __restrict__ rec, Ctrl* ctrl, u64* fp_out,
+                                                              u32* k_out, int nbx, int nby, int nbz) {
+  if (*(volatile int*)&ctrl->done) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Entry<3>* e = reinterpret_cast<Entry<3>*>(smem_raw);
+  __shared__ int any;
+  const i64 s0 = (i64)g.stride[0], s1 = (i64)g.stride[1];
+  const int ext0 = (int)((i64)g.nkeys / s0), ext1 = (int)(s0 / s1), ext2 = (int)s1;
+  const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
+  const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
+  const int tid = threadIdx.x;
+  if (tid == 0) any = 0;
+  __syncthreads();
+  // clear the previous table in this brick (its cells are no longer read)
+  for (int q = tid; q < kBrick * kBrick * kBrick; q += blockDim.x) {
+    const int z = z0 + q % kBrick, yv = y0 + (q / kBrick) % kBrick, x = x0 + q / (kBrick * kBrick);
+    if (x >= ext0 || yv >= ext1 || z >= ext2) continue;
+    Entry<3>* pe = prev.ent + (x * s0 + yv * s1 + z);
+    if (pe->count) {
+      pe->count = 0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) { pe->hi[j] = 0; pe->lo[j] = 0; }
+    }
+  }
+  // stage the halo (zeros outside the lattice)
+  int occ = 0;
+  for (int q = tid; q < kHalo * kHalo * kHalo; q += blockDim.x) {
+    const int hz = q % kHalo, hy = (q / kHalo) % kHalo, hx = q / (kHalo * kHalo);
+    const int x = x0 + hx - 1, yv = y0 + hy - 1, z = z0 + hz - 1;
+    Entry<3> v;
+    if (x >= 0 && yv >= 0 && z >= 0 && x < ext0 && yv < ext1 && z < ext2) {
+      v = tab.ent[x * s0 + yv * s1 + z];
+      if (hx >= 1 && hx <= kBrick && hy >= 1 && hy <= kBrick && hz >= 1 && hz <= kBrick) occ |= v.count != 0;
+    } else {
+      v.count = 0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) { v.hi[j] = 0; v.lo[j] = 0; }
+    }
+    e[q] = v;
+  }
+  if (occ) any = 1;
+  __syncthreads();
+  if (!any) return;
+  u64 fp = 0;
+  u32 kc = 0;
+  for (int q = tid; q < kBrick * kBrick * kBrick; q += blockDim.x) {
+    const int lz = q % kBrick, ly = (q / kBrick) % kBrick, lx = q / (kBrick * kBrick);
+    const int hc = ((lx + 1) * kHalo + (ly + 1)) * kHalo + (lz + 1);
+    const u64 own = e[hc].count;
+    if (own == 0) continue;
+    u64 cnt = 0;
+    i128 sum[3] = {0, 0, 0};
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx)
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dz = -1; dz <= 1; ++dz) {
+          const Entry<3>& nb = e[hc + (dx * kHalo + dy) * kHalo + dz];
+          cnt += nb.count;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) sum[j] += (((i128)(i64)nb.hi[j]) << 32) + (i128)nb.lo[j];
+        }
+    const u64 slot = (u64)(x0 + lx) * s0 + (u64)(y0 + ly) * s1 + (u64)(z0 + lz);
+    Rec<3> r;
+    const double c = (double)cnt;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) r.t[j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
+    bool inside;
+    r.key = pack_key<3>(g, r.t, inside);
+    if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+    rec[slot] = r;
+    fp += cell_fingerprint<3>(g, slot, own);
+    ++kc;
+  }
+  for (int o = 16; o; o >>= 1) {
+    fp += __shfl_xor_sync(kFull, fp, o);
+    kc += __shfl_xor_sync(kFull, kc, o);
+  }
+  if ((tid & 31) == 0) {
+    if (fp) atomicAdd((unsigned long long*)fp_out, (unsigned long long)fp);
+    if (kc) atomicAdd(k_out, kc);
+  }
+}
+
 // Table of y_{t+1} from the table of y_t.  Every point of occupied cell c
 // moves to exactly target_c (modeseek.py:109: y' depends on the cell only),
 // so the per-point histogram of y_{t+1} (grid.py:179-190) equals
