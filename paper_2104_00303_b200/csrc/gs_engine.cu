@@ -359,7 +359,11 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     });
     bricked = true;
   }
-  if (!bricked)
+  if (!bricked && D >= 4 && !Tab::kDense)
+    launch(c, K_AGG, [&] { k_agg_warp<D, Tab><<<c->sms * 8, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
+                                                    ctrl, cur, static_cast<u64*>(c->fp_hist.p) + t,
+                                                    static_cast<u32*>(c->k_hist.p) + t); });
+  else if (!bricked)
     launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur,
                                                     static_cast<u64*>(c->fp_hist.p) + t,
                                                     static_cast<u32*>(c->k_hist.p) + t); });
@@ -562,6 +566,20 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   const bool sorted = n >= kSortMinPoints;
   if (sorted)
     sinfo = p.dense ? spatial_sort<D>(c, p, tabs.dn, n) : spatial_sort<D>(c, p, tabs.hs, n);
+  if (sorted && !p.dense) {
+    // k never grows (k_{t+1} <= k_t: y_{t+1} takes at most k_t distinct
+    // values), so the loop's hash tables only need 2*k_0 slots: compact
+    // tables keep the 3^d probes in L2.  The buffers are clean, only the
+    // mask shrinks.
+    read_ctrl(c);
+    uint64_t cap = 256;
+    while (cap < 2ull * c->h_ctrl->nruns) cap <<= 1;
+    if (cap < p.slots) {
+      p.slots = cap;
+      p.g.mask = cap - 1;
+      tabs = make_tabs<D>(c, p);
+    }
+  }
   if (p.dense)
     enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
   else

@@ -672,6 +672,97 @@ __global__ void k_import_minima(Tab tab, const u32* kp, const u32* par, u32* fir
   }
 }
 
+// d >= 4 (81 or more neighbours): one warp per occupied cell, the lanes
+// split the 3^d offsets (independent probes in flight), then a warp
+// reduction of the exact 128-bit sums.
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Tab prev, Rec<D>* __restrict__ rec,
+                                                       Ctrl* ctrl, int cur, u64* fp_out, u32* k_out) {
+  if (*(volatile int*)&ctrl->done) return;
+  constexpr int M = (D == 1) ? 3 : (D == 2) ? 9 : (D == 3) ? 27 : (D == 4) ? 81 :
+                    (D == 5) ? 243 : (D == 6) ? 729 : (D == 7) ? 2187 : 6561;
+  const int lane = threadIdx.x & 31;
+  const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  {
+    const u32 kp = ctrl->k[cur ^ 1];
+    for (i64 a = tid; a < kp; a += stride) {
+      const u32 s = prev.list[a];
+      Entry<D>* e = prev.ent + s;
+      e->count = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) { e->hi[j] = 0; e->lo[j] = 0; }
+      if constexpr (!Tab::kDense) prev.keys[s] = kEmpty;
+    }
+  }
+  const i64 warp = tid >> 5;
+  const i64 nwarps = stride >> 5;
+  const u32 k = ctrl->k[cur];
+  u64 fp = 0;
+  u32 kc = 0;
+  for (i64 a = warp; a < k; a += nwarps) {
+    const u32 s = tab.list[a];
+    const u64 key = tab.key_of(s);
+    u64 cnt = 0;
+    u64 sh[D], sl[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { sh[j] = 0; sl[j] = 0; }
+    for (int o = lane; o < M; o += 32) {
+      int r = o;
+      i64 delta = 0;
+#pragma unroll
+      for (int j = D - 1; j >= 0; --j) {
+        delta += (i64)((r % 3) - 1) * (i64)g.stride[j];
+        r /= 3;
+      }
+      u32 ns;
+      if (tab.find(key + (u64)delta, ns)) {
+        const Entry<D>& e = tab.ent[ns];
+        cnt += e.count;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const i128 v = (((i128)(i64)e.hi[j]) << 32) + (i128)e.lo[j];
+          add128(sh[j], sl[j], (u64)((u128)v >> 64), (u64)v);
+        }
+      }
+    }
+    for (int off = 16; off; off >>= 1) {
+      cnt += __shfl_xor_sync(kFull, cnt, off);
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const u64 oh = __shfl_xor_sync(kFull, sh[j], off);
+        const u64 ol = __shfl_xor_sync(kFull, sl[j], off);
+        add128(sh[j], sl[j], oh, ol);
+      }
+    }
+    if (lane == 0) {
+      Rec<D> rr;
+      const double c = (double)cnt;
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        rr.t[j] = __ddiv_rn(i128_to_double((i128)((((u128)sh[j]) << 64) | (u128)sl[j]), -g.qexp[j]), c);
+      bool inside;
+      rr.key = pack_key<D>(g, rr.t, inside);
+      if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+      rec[s] = rr;
+      fp += cell_fingerprint<D>(g, key, tab.ent[s].count);
+      ++kc;
+    }
+  }
+  if (lane == 0) {
+    if (fp) atomicAdd((unsigned long long*)fp_out, (unsigned long long)fp);
+    if (kc) atomicAdd(k_out, kc);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctrl->agg_done, 1u) == gridDim.x - 1) {
+      ctrl->k[cur ^ 1] = 0;
+      ctrl->agg_done = 0;
+    }
+  }
+}
+
 // Dense 3-D tables: tiled 3x3x3 stencil.  A block owns an 8x8x8 brick of
 // lattice slots, stages the 10x10x10 halo of table entries in shared memory
 // once (~110 B of global reads per cell instead of 27 scattered entry
