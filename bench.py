@@ -43,7 +43,7 @@ UNIT = "point-updates/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=100_000_000, help="points (cfg4 default 1e8)")
@@ -83,10 +83,11 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            time.sleep(0.5)           # let the sampler come up before the timed region
         except OSError:
             self.proc = None
         return self
@@ -95,7 +96,10 @@ class Clocks:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == len(self.FIELDS):
-                self.samples.append(parts)
+                self.samples.append((time.time(), parts))
+
+    def window(self, t0, t1):
+        self.t0, self.t1 = t0, t1
 
     def __exit__(self, *exc):
         if self.proc:
@@ -106,14 +110,18 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", 1e30)
+        inside = [p for t, p in self.samples if t0 <= t <= t1]
+        samples = inside or [p for _, p in self.samples]
+        if not samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.samples = samples
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples), "in_timed_region": bool(inside)}
 
 
 # --------------------------------------------------------- CPU baseline
@@ -239,11 +247,13 @@ def our_arm(a):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        w0 = time.time()
         e0.record()
         for _ in range(a.steps):
             iters_total += step()
         e1.record()
         torch.cuda.synchronize()
+        clk.window(w0, time.time())
         barrier()
     ms = e0.elapsed_time(e1)
     if world == 1:   # sanity (untimed): labels dense in [0, k)
