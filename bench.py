@@ -301,6 +301,8 @@ def our_arm(a):
             "roofline": roof, "kernels": kernels, "gpu_launches": launches,
             "clocks": clk.summary()}
 
+    if rank == 0 and world == 1:
+        line["collapsed"] = collapsed_leg(gs, torch, x_dev, cfg, labels, n, a.steps)
     if rank == 0 and world == 1 and not a.no_e2e:
         line["e2e"] = e2e(x_host, cfg, n, min(a.steps, 3))
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -314,6 +316,29 @@ def our_arm(a):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def collapsed_leg(gs, torch, x_dev, cfg, labels, n, steps):
+    """Same workload, iterations t >= 1 in the collapsed-group formulation
+    (SURVEY 8f rank 1): bit-identical results, but iterations move one
+    position per run of identical points instead of every point -- reported
+    beside, never as, the per-point metric."""
+    gs.meanshiftpp_device(x_dev, cfg, labels, collapsed=True)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    it = 0
+    e0.record()
+    for _ in range(steps):
+        it += gs.meanshiftpp_device(x_dev, cfg, labels, collapsed=True)[2]
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"value": n * it / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps,
+            "note": "collapsed-group formulation (SURVEY.md 8f rank 1): after iteration 0 each run of "
+                    "identical points moves as one; results bit-identical to the per-point engine "
+                    "(tests/test_gpu_parity.py::test_collapsed_mode_bit_identical); not a per-point "
+                    "workload, so not the headline"}
 
 
 def e2e(x_host, cfg, n, steps):

@@ -103,6 +103,15 @@ GS_API int gs_segment_image(gs_ctx* ctx, const uint8_t* pixels, int32_t height, 
                      int64_t* labels_out, int64_t* k_out, int32_t* iters_out,
                      double* movement_out, int32_t* converged_out);
 
+/* Context options.  GS_OPT_COLLAPSED (0/1, default 0): run iterations
+ * t >= 1 of gs_meanshiftpp* in the collapsed-group formulation (SURVEY.md
+ * 8f): after iteration 0 all points of a run of the spatial sort share one
+ * position, so each iteration updates one position per run (the tables and
+ * movement are the same exact integers; results are bit-identical).  The
+ * per-point iterate is then not materialised after iteration 0. */
+#define GS_OPT_COLLAPSED 1
+GS_API int gs_ctx_set_option(gs_ctx* ctx, int32_t option, int64_t value);
+
 /* Modes (k, d) of the last run on this context (Labeling.modes). */
 GS_API int gs_fetch_modes(gs_ctx* ctx, double* modes_out, int64_t cap_rows);
 

@@ -19,6 +19,7 @@ LIB_PATH = Path(os.environ.get("GRIDSHIFT_LIB", Path(__file__).resolve().parent 
 
 GS_OK, GS_EINVAL, GS_ERUNTIME, GS_EUNSUPPORTED = 0, 1, 2, 3
 GS_DTYPE_F64, GS_DTYPE_F32 = 0, 1
+GS_OPT_COLLAPSED = 1
 
 _P = C.c_void_p
 _i32 = C.c_int32
@@ -37,6 +38,7 @@ SIGNATURES = {
     "gs_segment_image": (C.c_int, [_P, _P, _i32, _i32, _i32, _f64, _f64, _f64, _i32, _P, _P, _P,
                                    _P, _P]),
     "gs_fetch_modes": (C.c_int, [_P, _P, _i64]),
+    "gs_ctx_set_option": (C.c_int, [_P, _i32, _i64]),
     "gs_fetch_trace": (C.c_int, [_P, _P, _P, _i32]),
     "gs_profile": (C.c_int, [_P, _i32, _P, _P, _i32]),
     "gs_profile_kind": (C.c_char_p, [_i32]),

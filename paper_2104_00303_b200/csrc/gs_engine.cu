@@ -90,6 +90,8 @@ struct gs_ctx {
   std::vector<uint64_t> iter_fp;
   std::vector<int64_t> track_bins;
   Prof prof;
+  bool collapsed = false;               // option: collapsed iterations (gs_ctx_set_option)
+  Buf runposb, runcntb;
   struct ShardState* shard = nullptr;   // row-sharded run in progress (gs_shard_*)
 };
 
@@ -317,6 +319,10 @@ struct SortInfo {
   u32* minidx = nullptr;    // per initial slot: smallest original index
   u32* runs = nullptr;      // occupied initial slots
   u32* runroot = nullptr;   // per initial slot: final component root (scratch)
+  u32* end = nullptr;       // per initial slot: run end (the scatter cursors)
+  double* runpos = nullptr; // collapsed mode: per-run positions (SoA, ld = rld)
+  u32* runcnt = nullptr;
+  int64_t rld = 0;
 };
 
 // -------------------------------------------------------------- iteration
@@ -334,7 +340,7 @@ void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_p
 // the table of y_{t+1} from it (O(cells)), k_shift moves every point.
 template <int D, class Tab>
 void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, int64_t n, int nb_pts,
-                       int nb_cells, u64* limbs = nullptr) {
+                       int nb_cells, u64* limbs = nullptr, bool with_shift = true) {
   const int cur = t & 1;
   double* y_in = static_cast<double*>(c->y[cur].p);
   double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
@@ -369,9 +375,26 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
                                                     static_cast<u32*>(c->k_hist.p) + t); });
   launch(c, K_DERIVE, [&] { k_derive<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
                                                                                 ctrl, cur); });
-  launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec, ctrl,
+  if (with_shift)
+    launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec, ctrl,
                                                   static_cast<u64*>(c->partials.p),
                                                   static_cast<double*>(c->mv_hist.p), t, eta, limbs); });
+}
+
+// Collapsed iteration t >= 1: targets + derived table as usual, then one
+// position update per run (k_run_shift) instead of the per-point shift.
+template <int D, class Tab>
+void enqueue_run_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, const SortInfo& si,
+                           int nb_cells) {
+  const int cur = t & 1;
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  Rec<D>* rec = static_cast<Rec<D>*>(c->targets.p);
+  enqueue_iteration<D>(c, p, tabs, t, eta, 0, 1, nb_cells, nullptr, false);   // agg + derive only
+  launch(c, K_SHIFT, [&] {
+    k_run_shift<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(si.runpos, si.runcnt, &ctrl->nruns, si.rld, p.g,
+                                                           tabs[cur], rec, ctrl, static_cast<u64*>(c->partials.p),
+                                                           static_cast<double*>(c->mv_hist.p), t, eta);
+  });
 }
 
 // Occupied-cell list of a table (hash tables maintain theirs on insert;
@@ -423,7 +446,8 @@ void extract_components(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, i
   if (si)
     launch(c, K_LABELS, [&] {
       k_run_first<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(yf, p.g, tabs[e], si->runs, &ctrl->nruns, si->start,
-                                                            si->minidx, par, first, si->runroot, ctrl, offset);
+                                                            si->minidx, par, first, si->runroot, ctrl, offset,
+                                                            si->runpos, si->rld);
     });
   else
     launch(c, K_LABELS, [&] {
@@ -510,7 +534,8 @@ SortInfo spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   si.minidx = ensure<u32>(c, c->runmin, p.slots);
   si.runs = ensure<u32>(c, c->runlist, p.list_cap);
   si.cell0 = ensure<u32>(c, c->cell0, (size_t)n);
-  si.runroot = off;   // the cursors are dead once the scatter is done
+  si.runroot = off;   // the cursors are dead once the scatter is done...
+  si.end = off;       // ...except as run ends, read (collapsed mode) before runroot is written
   GS_CUDA(cudaMemsetAsync(si.minidx, 0xff, p.slots * sizeof(u32), c->st));
   double* y0 = static_cast<double*>(c->y[0].p);
   double* y1 = static_cast<double*>(c->y[1].p);
@@ -584,15 +609,38 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
     enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
   else
     enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts);
+  // collapsed mode: after iteration 0 the runs of the spatial
+  // sort hold one position each; later iterations move runs, not points
+  const bool collapsed = c->collapsed && sorted && max_iters > 1;
+  if (collapsed) {
+    sinfo.rld = (int64_t)((p.list_cap + 127) & ~uint64_t(127));
+    sinfo.runpos = ensure<double>(c, c->runposb, (size_t)sinfo.rld * D);
+    sinfo.runcnt = ensure<u32>(c, c->runcntb, p.list_cap);
+  }
   // device-driven loop: enqueue chunks, synchronise between chunks only
   int t = 0, chunk = 4;
   while (t < max_iters) {
     const int m = std::min(chunk, max_iters - t);
     for (int q = 0; q < m; ++q, ++t) {
+      if (collapsed && t >= 1) {
+        if (p.dense)
+          enqueue_run_iteration<D>(c, p, tabs.dn, t, eta, sinfo, nb_cells);
+        else
+          enqueue_run_iteration<D>(c, p, tabs.hs, t, eta, sinfo, nb_cells);
+        continue;
+      }
       if (p.dense)
         enqueue_iteration<D>(c, p, tabs.dn, t, eta, n, nb_pts, nb_cells);
       else
         enqueue_iteration<D>(c, p, tabs.hs, t, eta, n, nb_pts, nb_cells);
+      if (collapsed && t == 0) {
+        Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+        const double* y1 = static_cast<const double*>(c->y[1].p);
+        launch(c, K_SHIFT, [&] {
+          k_runs_gather<D><<<nb_cells, kThreads, 0, c->st>>>(y1, p.g.ld, sinfo.runs, &ctrl->nruns, sinfo.start,
+                                                              sinfo.end, sinfo.runpos, sinfo.runcnt, sinfo.rld);
+        });
+      }
     }
     check_launch();
     read_ctrl(c);
@@ -942,7 +990,7 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
                  &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
-                 &c->runlist, &c->cell0, &c->stage};
+                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
@@ -1009,6 +1057,15 @@ int gs_segment_image(gs_ctx* c, const uint8_t* pixels, int32_t height, int32_t w
     if (k_out) *k_out = r.k;
     if (iters_out) *iters_out = r.iters;
     if (converged_out) *converged_out = r.converged;
+  });
+}
+
+int gs_ctx_set_option(gs_ctx* c, int32_t option, int64_t value) {
+  return guarded(c, [&] {
+    if (option == GS_OPT_COLLAPSED)
+      c->collapsed = value != 0;
+    else
+      fail(GS_EINVAL, "unknown option");
   });
 }
 

@@ -640,6 +640,90 @@ __global__ void __launch_bounds__(kThreads, 3) k_shift(const double* __restrict_
   }
 }
 
+// Collapsed formulation: after iteration 0 all points of a run
+// (initial cell) share one position, so iterations t >= 1 move one position
+// per run.  runpos: SoA (D x R) positions, runcnt: points per run.  The
+// movement is count * fixed(norm) per run -- the same exact integer as the
+// per-point sum, so every result is bit-identical to the per-point path.
+template <int D>
+__global__ void k_runs_gather(const double* __restrict__ y, i64 ld, const u32* runs, const u32* nruns,
+                              const u32* start, const u32* end, double* runpos, u32* runcnt, i64 rld) {
+  const u32 R = *nruns;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
+    const u32 s0 = runs[r];
+    const u32 p = start[s0];
+#pragma unroll
+    for (int j = 0; j < D; ++j) runpos[(i64)j * rld + r] = y[(i64)j * ld + p];
+    runcnt[r] = end[s0] - p;
+  }
+}
+
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_run_shift(double* __restrict__ runpos, const u32* __restrict__ runcnt,
+                                                        const u32* nruns, i64 rld, GridParams g, Tab tab,
+                                                        const Rec<D>* __restrict__ rec, Ctrl* ctrl, u64* partials,
+                                                        double* mv_hist, int t, double eta) {
+  if (*(volatile int*)&ctrl->done) return;
+  const u32 R = *nruns;
+  u64 ahi = 0, alo = 0;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
+    double v[D], o[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = runpos[(i64)j * rld + r];
+    const Rec<D>& rr = lookup_rec<D>(g, tab, rec, v, ctrl);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      o[j] = rr.t[j];
+      runpos[(i64)j * rld + r] = o[j];
+    }
+    const u128 f = move_fixed<D>(g, o, v) * (u128)runcnt[r];
+    add128(ahi, alo, (u64)(f >> 64), (u64)f);
+  }
+  const int lane = threadIdx.x & 31;
+  for (int off = 16; off; off >>= 1) {
+    const u64 oh = __shfl_xor_sync(kFull, ahi, off);
+    const u64 ol = __shfl_xor_sync(kFull, alo, off);
+    add128(ahi, alo, oh, ol);
+  }
+  __shared__ u64 sh[kThreads / 32][2];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5;
+  if (lane == 0) { sh[w][0] = ahi; sh[w][1] = alo; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 bh = 0, bl = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    partials[2 * blockIdx.x] = bh;
+    partials[2 * blockIdx.x + 1] = bl;
+    __threadfence();
+    last = (atomicAdd(&ctrl->blocks_done, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  u64 th = 0, tl = 0;
+  for (u32 b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+    add128(th, tl, __ldcg(partials + 2 * b), __ldcg(partials + 2 * b + 1));
+  for (int off = 16; off; off >>= 1) {
+    const u64 oh = __shfl_xor_sync(kFull, th, off);
+    const u64 ol = __shfl_xor_sync(kFull, tl, off);
+    add128(th, tl, oh, ol);
+  }
+  __syncthreads();
+  if (lane == 0) { sh[w][0] = th; sh[w][1] = tl; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 bh = 0, bl = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) add128(bh, bl, sh[q][0], sh[q][1]);
+    ctrl->blocks_done = 0;
+    const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
+    mv_hist[t] = mv;
+    ctrl->iters = t + 1;
+    if (mv < eta) ctrl->done = 1;
+  }
+}
+
 // Sharded run: global movement from the all-reduced limbs (exact).
 __global__ void k_converge(const u64* limbs, GridParams g, Ctrl* ctrl, double* mv_hist, int t, double eta) {
   if (*(volatile int*)&ctrl->done) return;
@@ -1220,15 +1304,20 @@ __global__ void __launch_bounds__(kThreads) k_unstage(const double* __restrict__
 template <int D, class Tab>
 __global__ void k_run_first(const double* __restrict__ yf, GridParams g, Tab tab, const u32* runs,
                             const u32* nruns, const u32* start, const u32* minidx, const u32* par,
-                            u32* first, u32* runroot, Ctrl* ctrl, u32 offset) {
+                            u32* first, u32* runroot, Ctrl* ctrl, u32 offset, const double* runpos, i64 rld) {
   const u32 R = *nruns;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < R; a += stride) {
     const u32 s0 = runs[a];
-    const u32 p = start[s0];
     double v[D];
+    if (runpos) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) v[j] = yf[(i64)j * g.ld + p];
+      for (int j = 0; j < D; ++j) v[j] = runpos[(i64)j * rld + a];
+    } else {
+      const u32 p = start[s0];
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = yf[(i64)j * g.ld + p];
+    }
     bool inside;
     const u64 key = pack_key<D>(g, v, inside);
     u32 sf = 0;

@@ -117,11 +117,13 @@ def meanshiftpp(points: PointSet, cfg: ShiftConfig, labels_out: np.ndarray | Non
     return _finish(ctx, labels, int(k.value), d, int(it.value), mv, conv.value)
 
 
-def meanshiftpp_device(x, cfg: ShiftConfig, labels_out=None, stream=None):
+def meanshiftpp_device(x, cfg: ShiftConfig, labels_out=None, stream=None, collapsed: bool = False):
     """Device-resident entry: `x` is a CUDA tensor (n, d) float64 or float32
     (anything exposing data_ptr()).  Labels are written into `labels_out`
     (CUDA int64 tensor, allocated if None).  Returns (labels_out, k, iters,
-    movement, converged); modes via `last_modes()`."""
+    movement, converged); modes via `last_modes()`.  collapsed=True runs
+    iterations t >= 1 per run of identical points (bit-identical
+    results, not a per-point workload)."""
     import torch
 
     L = _lib.load()
@@ -139,10 +141,12 @@ def meanshiftpp_device(x, cfg: ShiftConfig, labels_out=None, stream=None):
     mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
     k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
     s = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+    _lib.check(L.gs_ctx_set_option(ctx, _lib.GS_OPT_COLLAPSED, 1 if collapsed else 0))
     _lib.check(L.gs_meanshiftpp_device(ctx, C.c_void_p(x.data_ptr()), dtype, n, d, float(cfg.h),
                                        eta, int(cfg.max_iters), C.c_void_p(labels_out.data_ptr()),
                                        _lib.ref(k), _lib.ref(it), _lib.ptr(mv), _lib.ref(conv),
                                        C.c_void_p(s)))
+    _lib.check(L.gs_ctx_set_option(ctx, _lib.GS_OPT_COLLAPSED, 0))
     return labels_out, int(k.value), int(it.value), mv[: it.value].copy(), bool(conv.value)
 
 

@@ -328,3 +328,34 @@ def test_cfg1_exact_model_bitwise():
     c = W.CONFIGS["cfg1"]
     lab, tr = gs.segment_pixels(gs.Image(W.cfg1_image()), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]), "rgb")
     _check_model(lab, tr, f, c["h"])
+
+
+# ------------------------------------------------- collapsed formulation
+
+@pytest.mark.parametrize("case", ["cloud", "rgb", "rgbxy", "blobs"])
+def test_collapsed_mode_bit_identical(case):
+    # iterations t >= 1 per run of identical points; the
+    # tables / movement are the same exact integers -> identical results
+    import torch
+
+    if case == "cloud":
+        x, cfg = W.cloud3d(300_000, seed=31).astype(np.float64), gs.ShiftConfig(1.0, 1e-3, 30)
+    elif case == "rgb":
+        x = gs.image_to_features(gs.Image(W.voronoi_image(400, 300, 20, seed=4)), "rgb").data
+        cfg = gs.ShiftConfig(8.0, 1e-3, 100)
+    elif case == "rgbxy":
+        x = gs.image_to_features(gs.Image(W.voronoi_image(400, 300, 20, seed=5)), "rgbxy", 0.25).data
+        cfg = gs.ShiftConfig(10.0, 1e-3, 100)
+    else:
+        x, cfg = W.blobs2d(100_000, seed=2), gs.ShiftConfig(0.5, 1e-4, 300)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    a, ka, ia, ma, ca = gs.meanshiftpp_device(xd, cfg)
+    a = a.cpu().numpy()
+    moda = gs.modeseek.last_modes(ka, x.shape[1])
+    b, kb, ib, mb, cb = gs.meanshiftpp_device(xd, cfg, collapsed=True)
+    b = b.cpu().numpy()
+    modb = gs.modeseek.last_modes(kb, x.shape[1])
+    assert (ka, ia, ca) == (kb, ib, cb)
+    assert np.array_equal(a, b)
+    assert np.array_equal(moda, modb)
+    np.testing.assert_array_equal(ma, mb)
