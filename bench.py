@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-kernels", action="store_true", default=True)
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the row-sharded (NCCL) engine even at one rank (tests the N>1 path)")
     return ap.parse_args()
 
 
@@ -209,17 +211,23 @@ def our_arm(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     os.environ["GRIDSHIFT_DEVICE"] = str(local)
-    if world > 1:
+    shard = world > 1 or a.force_sharded
+    if shard:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     h, eta, mi = cfg4()
     n = a.n
     x_host = W.cloud3d(n)                       # fp32 (n, 3), seeded
-    if world > 1:
+    if shard:
         from paper_2104_00303_b200 import sharded
 
         lo, hi = sharded.shard_bounds(n, world, rank)
         x_dev = torch.from_numpy(x_host[lo:hi]).cuda()
     else:
+        lo, hi = 0, n
         x_dev = torch.from_numpy(x_host).cuda()
     cfg = gs.ShiftConfig(h=h, eta=eta, max_iters=mi)
     labels = torch.empty(x_dev.shape[0], dtype=torch.int64, device="cuda")
@@ -227,14 +235,14 @@ def our_arm(a):
     last = {}
 
     def step():
-        if world > 1:
+        if shard:
             return sharded.meanshiftpp_sharded(x_dev, cfg, labels, n_total=n)
         _, k, it, mv, conv = gs.meanshiftpp_device(x_dev, cfg, labels)
         last["k"] = k
         return it
 
     def barrier():
-        if world > 1:
+        if shard:
             dist.barrier()
 
     for _ in range(max(3, a.warmup)):
@@ -256,12 +264,12 @@ def our_arm(a):
         clk.window(w0, time.time())
         barrier()
     ms = e0.elapsed_time(e1)
-    if world == 1:   # sanity (untimed): labels dense in [0, k)
+    if not shard:   # sanity (untimed): labels dense in [0, k)
         u = torch.unique(labels)
         assert int(u[0]) == 0 and int(u[-1]) == last["k"] - 1 and u.numel() == last["k"], "bad labels"
     prof = _lib.profile(2)
     _lib.profile(0)
-    if world > 1:
+    if shard:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -301,17 +309,24 @@ def our_arm(a):
             "roofline": roof, "kernels": kernels, "gpu_launches": launches,
             "clocks": clk.summary()}
 
-    if rank == 0 and world == 1:
+    if shard:
+        line["config"]["parallelism"] = f"rows sharded over {world} GPU(s), NCCL"
+    if rank == 0 and not shard:
         line["collapsed"] = collapsed_leg(gs, torch, x_dev, cfg, labels, n, a.steps)
-    if rank == 0 and world == 1 and not a.no_e2e:
-        line["e2e"] = e2e(x_host, cfg, n, min(a.steps, 3))
+    if not a.no_e2e:
+        if shard:
+            e = e2e_sharded(sharded, dist, torch, x_host[lo:hi], cfg, n, min(a.steps, 3))
+            if rank == 0:
+                line["e2e"] = e
+        elif rank == 0:
+            line["e2e"] = e2e(x_host, cfg, n, min(a.steps, 3))
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         x, iters, what = cpu_sample(n, 12.0, x_host)
         ups, secs, it = run_oracle(x, iters)
         line["cpu_baseline"] = {"value": ups / secs, "unit": UNIT, "cores": 1, "kind": "port",
                                 "sample": f"{what} (uniform random subsample), {it} iterations, "
                                           f"oracle/gridshift_oracle.py (numpy, single-threaded)"}
-    if world > 1:
+    if shard:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
@@ -339,6 +354,35 @@ def collapsed_leg(gs, torch, x_dev, cfg, labels, n, steps):
                     "identical points moves as one; results bit-identical to the per-point engine "
                     "(tests/test_gpu_parity.py::test_collapsed_mode_bit_identical); not a per-point "
                     "workload, so not the headline"}
+
+
+def e2e_sharded(sharded, dist, torch, x_shard, cfg, n, steps):
+    """N-GPU end to end through the sharded public entry: every step copies
+    this rank's rows (fp64, pinned host) to its GPU, runs the sharded engine
+    and copies its labels back; time = max over ranks."""
+    pts = torch.empty((x_shard.shape[0], 3), dtype=torch.float64, pin_memory=True)
+    pts.numpy()[:] = x_shard
+    lab_host = torch.empty(x_shard.shape[0], dtype=torch.int64, pin_memory=True)
+    x_dev = torch.empty_like(pts, device="cuda")
+    labels = torch.empty(x_shard.shape[0], dtype=torch.int64, device="cuda")
+
+    def one():
+        x_dev.copy_(pts, non_blocking=True)
+        it = sharded.meanshiftpp_sharded(x_dev, cfg, labels, n_total=n)
+        lab_host.copy_(labels, non_blocking=True)
+        torch.cuda.synchronize()
+        return it
+
+    one()
+    dist.barrier()
+    t0 = time.perf_counter()
+    it = sum(one() for _ in range(steps))
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    secs = float(dt.item())
+    return {"value": n * it / secs, "unit": UNIT, "h2d_bytes_per_step": int(pts.numel() * 8),
+            "d2h_bytes_per_step": int(lab_host.numel() * 8), "steps": steps,
+            "api": "paper_2104_00303_b200.sharded.meanshiftpp_sharded (per-rank H2D/D2H, max over ranks)"}
 
 
 def e2e(x_host, cfg, n, steps):
