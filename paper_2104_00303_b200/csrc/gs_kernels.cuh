@@ -1362,8 +1362,10 @@ __global__ void __launch_bounds__(kThreads) k_labels_runs(const u32* __restrict_
                                                           const u32* __restrict__ runroot,
                                                           const u32* __restrict__ rankmap, i64* labels) {
   const i64 stride = (i64)gridDim.x * blockDim.x;
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    labels[i] = (i64)rankmap[runroot[cell0[i]]];
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 s0 = cell0[i];   // 0xffffffff only after a flagged lookup failure
+    labels[i] = s0 == 0xffffffffu ? -1 : (i64)rankmap[runroot[s0]];
+  }
 }
 
 // ------------------------------------------------------------- extraction
