@@ -83,6 +83,14 @@ GS_API int gs_meanshiftpp(gs_ctx* ctx, const double* x, int64_t n, int32_t d, do
                    int32_t max_iters, int64_t* labels_out, int64_t* k_out, int32_t* iters_out,
                    double* movement_out, int32_t* converged_out);
 
+/* Host input in float64 or float32 (GS_DTYPE_*): float32 rows are copied
+ * as-is and upcast on device, exactly as PointSet upcasts on the host
+ * (grid.py:43) -- half the host->device bytes for float32 data. */
+GS_API int gs_meanshiftpp_host(gs_ctx* ctx, const void* x, int32_t dtype, int64_t n, int32_t d,
+                               double h, double eta, int32_t max_iters, int64_t* labels_out,
+                               int64_t* k_out, int32_t* iters_out, double* movement_out,
+                               int32_t* converged_out);
+
 /* Same engine on device-resident input (x_dev: (n,d) row-major, dtype
  * GS_DTYPE_F64 or GS_DTYPE_F32 -- f32 is upcast on device as PointSet
  * does on the host, grid.py:43).  labels_dev: (n,) int64 device buffer.

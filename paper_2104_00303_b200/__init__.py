@@ -10,7 +10,7 @@ does, and raises if it is missing -- there is no CPU fallback.
 from .grid import (CellTables, PointSet, bin_point, bin_points, build_cell_tables,
                    neighbor_aggregate, neighbor_stats)
 from .modeseek import (ENGINES, Labeling, ShiftConfig, ShiftTrace, extract_clusters, install,
-                       meanshiftpp, meanshiftpp_device, meanshiftpp_step)
+                       meanshiftpp, meanshiftpp_device, meanshiftpp_points, meanshiftpp_step)
 from .segment import Image, SegmentMap, image_to_features, segment_image, segment_pixels
 from .track import (BinSet, TrackState, Window, cluster_window, init_tracker, neighborhood,
                     track_frame, track_sequence)
@@ -19,7 +19,7 @@ __all__ = [
     "BinSet", "CellTables", "ENGINES", "Image", "Labeling", "PointSet", "SegmentMap",
     "ShiftConfig", "ShiftTrace", "TrackState", "Window", "bin_point", "bin_points",
     "build_cell_tables", "cluster_window", "extract_clusters", "image_to_features",
-    "init_tracker", "install", "meanshiftpp", "meanshiftpp_device", "meanshiftpp_step",
+    "init_tracker", "install", "meanshiftpp", "meanshiftpp_device", "meanshiftpp_points", "meanshiftpp_step",
     "neighbor_aggregate", "neighbor_stats", "neighborhood", "segment_image", "segment_pixels",
     "track_frame", "track_sequence",
 ]

@@ -33,6 +33,7 @@ SIGNATURES = {
     "gs_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "gs_ctx_destroy": (None, [_P]),
     "gs_meanshiftpp": (C.c_int, [_P, _P, _i64, _i32, _f64, _f64, _i32, _P, _P, _P, _P, _P]),
+    "gs_meanshiftpp_host": (C.c_int, [_P, _P, _i32, _i64, _i32, _f64, _f64, _i32, _P, _P, _P, _P, _P]),
     "gs_meanshiftpp_device": (C.c_int, [_P, _P, _i32, _i64, _i32, _f64, _f64, _i32, _P, _P, _P,
                                         _P, _P, _P]),
     "gs_segment_image": (C.c_int, [_P, _P, _i32, _i32, _i32, _f64, _f64, _f64, _i32, _P, _P, _P,

@@ -1020,6 +1020,27 @@ int gs_meanshiftpp(gs_ctx* c, const double* x, int64_t n, int32_t d, double h, d
   });
 }
 
+int gs_meanshiftpp_host(gs_ctx* c, const void* x, int32_t dtype, int64_t n, int32_t d, double h, double eta,
+                        int32_t max_iters, int64_t* labels_out, int64_t* k_out, int32_t* iters_out,
+                        double* movement_out, int32_t* converged_out) {
+  return guarded(c, [&] {
+    validate_run(n, d, h, eta, max_iters);
+    if (!x || !labels_out) fail(GS_EINVAL, "null buffer");
+    if (dtype != GS_DTYPE_F64 && dtype != GS_DTYPE_F32) fail(GS_EINVAL, "dtype must be f64 or f32");
+    const size_t esz = dtype == GS_DTYPE_F64 ? 8 : 4;
+    unsigned char* dx = ensure<unsigned char>(c, c->x_stage, (size_t)n * d * esz);
+    GS_CUDA(cudaMemcpyAsync(dx, x, (size_t)n * d * esz, cudaMemcpyHostToDevice, c->st));
+    int64_t* dl = ensure<int64_t>(c, c->labels, n);
+    Input in{dtype == GS_DTYPE_F64 ? IN_F64 : IN_F32, dx};
+    RunOut r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
+    GS_CUDA(cudaMemcpyAsync(labels_out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (k_out) *k_out = r.k;
+    if (iters_out) *iters_out = r.iters;
+    if (converged_out) *converged_out = r.converged;
+  });
+}
+
 int gs_meanshiftpp_device(gs_ctx* c, const void* x_dev, int32_t dtype, int64_t n, int32_t d, double h,
                           double eta, int32_t max_iters, int64_t* labels_dev, int64_t* k_out,
                           int32_t* iters_out, double* movement_out, int32_t* converged_out, void* stream) {

@@ -131,6 +131,31 @@ def meanshiftpp(points: PointSet, cfg: ShiftConfig, labels_out: np.ndarray | Non
     return _finish(ctx, labels, int(k.value), d, int(it.value), mv, conv.value)
 
 
+def meanshiftpp_points(x: np.ndarray, cfg: ShiftConfig, labels_out: np.ndarray | None = None
+                       ) -> tuple[Labeling, ShiftTrace]:
+    """meanshiftpp on a raw host (n, d) array of float32 or float64 without
+    building a PointSet: float32 rows cross PCIe as float32 and are upcast on
+    device -- bit-identical to PointSet's host upcast (grid.py:43) at half
+    the transfer.  Validation (finite, n, d >= 1) happens on device."""
+    x = np.asarray(x)
+    if x.dtype not in (np.float32, np.float64):
+        x = x.astype(np.float64)
+    x = np.ascontiguousarray(x)
+    if x.ndim != 2:
+        raise ValueError(f"point data must be 2-d (n, d), got shape {x.shape}")
+    L = _lib.load()
+    ctx = _lib.context()
+    n, d = x.shape
+    eta = cfg.resolve_eta(n)
+    labels = np.empty(n, dtype=np.int64) if labels_out is None else labels_out
+    mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
+    k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
+    dt = _lib.GS_DTYPE_F32 if x.dtype == np.float32 else _lib.GS_DTYPE_F64
+    _lib.check(L.gs_meanshiftpp_host(ctx, _lib.ptr(x), dt, n, d, float(cfg.h), eta, int(cfg.max_iters),
+                                     _lib.ptr(labels), _lib.ref(k), _lib.ref(it), _lib.ptr(mv), _lib.ref(conv)))
+    return _finish(ctx, labels, int(k.value), d, int(it.value), mv, conv.value)
+
+
 def meanshiftpp_device(x, cfg: ShiftConfig, labels_out=None, stream=None, collapsed: bool = False):
     """Device-resident entry: `x` is a CUDA tensor (n, d) float64 or float32
     (anything exposing data_ptr()).  Labels are written into `labels_out`

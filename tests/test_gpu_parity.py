@@ -359,3 +359,16 @@ def test_collapsed_mode_bit_identical(case):
     assert np.array_equal(a, b)
     assert np.array_equal(moda, modb)
     np.testing.assert_array_equal(ma, mb)
+
+
+def test_points_api_float32_equals_pointset_upcast():
+    x32 = W.cloud3d(200_000, seed=51)
+    cfg = gs.ShiftConfig(1.0, 1e-3, 20)
+    a, ta = gs.meanshiftpp_points(x32, cfg)
+    b, tb = gs.meanshiftpp(gs.PointSet(x32), cfg)      # PointSet upcasts on the host
+    assert np.array_equal(a.labels, b.labels) and np.array_equal(a.modes, b.modes)
+    np.testing.assert_array_equal(ta.total_movement_per_iter, tb.total_movement_per_iter)
+    bad = x32[:10].copy()
+    bad[3, 1] = np.nan
+    with pytest.raises(ValueError):
+        gs.meanshiftpp_points(bad, cfg)
