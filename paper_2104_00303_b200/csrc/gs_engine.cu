@@ -91,7 +91,7 @@ struct gs_ctx {
   std::vector<int64_t> track_bins;
   Prof prof;
   bool collapsed = false;               // option: collapsed iterations (gs_ctx_set_option)
-  Buf runposb, runcntb;
+  Buf runposb, runcntb, bkcnt, bktot;
   struct ShardState* shard = nullptr;   // row-sharded run in progress (gs_shard_*)
 };
 
@@ -517,10 +517,13 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
   extract_finish<D>(c, p, tabs, yf, n, e, labels_dev, si);
 }
 
-// One-time counting sort of the iterate by initial cell (see k_scatter).
-// Leaves table buffer 0 clean; y[0] holds the sorted iterate afterwards.
+// One-time counting sort of the iterate by initial cell.
+// Dense tables: the two-level sort (k_bk_*), which also leaves table buffer 0
+// holding the table of y_0 (built from shared-memory tallies) and returns
+// true.  Hash tables: per-point cursor scatter (k_scatter); table buffer 0
+// is left clean and false returned.  y[0] holds the sorted iterate after.
 template <int D, class Tab>
-SortInfo spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
+bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   // dense: scan every slot in key order (lexicographic cell order);
@@ -528,7 +531,6 @@ SortInfo spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   const u64 nitems = Tab::kDense ? p.slots : p.list_cap;
   const int nbs = (int)((nitems + kScanChunk - 1) / kScanChunk);
   u64* bsum = ensure<u64>(c, c->scan, (size_t)nbs + 1);
-  SortInfo si;
   u32* off = ensure<u32>(c, c->runoff, p.slots);
   si.start = ensure<u32>(c, c->runstart, p.slots);
   si.minidx = ensure<u32>(c, c->runmin, p.slots);
@@ -540,26 +542,58 @@ SortInfo spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n) {
   double* y0 = static_cast<double*>(c->y[0].p);
   double* y1 = static_cast<double*>(c->y[1].p);
   const u32* list = Tab::kDense ? nullptr : tabs[0].list;
-  launch(c, K_SORT, [&] { k_hist<D, Tab, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
   if constexpr (Tab::kDense) {
+    // coarse buckets of 2^shift consecutive slots, at most 2048 of them
+    int shift = 10;
+    while ((p.slots >> shift) >= 2048) ++shift;
+    const u32 nb = (u32)((p.slots + (1ull << shift) - 1) >> shift);
+    const u32 nblk = (u32)c->sms * 8;
+    const int64_t chunk = (n + nblk - 1) / nblk;
+    u32* bk = ensure<u32>(c, c->bkcnt, (size_t)nblk * nb);
+    u64* btot = ensure<u64>(c, c->bktot, (size_t)nb + 1);
+    double* stage = ensure<double>(c, c->stage, (size_t)n * StRec<D>::W);
+    const size_t st_smem = bk_stage_smem<D>(nb);
+    static bool attr = false;
+    if (!attr) {
+      GS_CUDA(cudaFuncSetAttribute(k_bk_stage<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_stage_smem<D>(2048)));
+      attr = true;
+    }
+    const int nch = (int)((n + kChunkRecs - 1) / kChunkRecs);
+    GS_CUDA(cudaMemsetAsync(off, 0, p.slots * sizeof(u32), c->st));
+    launch(c, K_SORT, [&] { k_bk_count<D><<<nblk, kThreads, nb * sizeof(u32), c->st>>>(y0, n, p.g, shift, nb, chunk, bk, si.cell0, ctrl); });
+    launch(c, K_SORT, [&] { k_bk_cols<<<nb, 1024, 0, c->st>>>(bk, nblk, nb, btot); });
+    launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(btot, (int)nb); });
+    launch(c, K_SORT, [&] { k_bk_stage<D><<<nblk, 512, st_smem, c->st>>>(y0, n, p.g, shift, nb, chunk, bk, btot, si.cell0, stage); });
+    launch(c, K_SORT, [&] { k_bk_tally<D><<<nch, 512, 0, c->st>>>(stage, n, p.slots, off, si.minidx, ctrl); });
+    launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, p.slots, off); });
+    launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
+    launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, off, p.slots, si.start, off); });
+    launch(c, K_SORT, [&] { k_bk_place<D><<<nch, 512, 0, c->st>>>(stage, n, p.slots, p.g, off, y1); });
+    std::swap(c->y[0], c->y[1]);
+    // table 0 from the sorted iterate (runs are contiguous: cheap), then the
+    // occupied-slot list of the runs
+    enqueue_first_hist<D>(c, p, tabs, n, nb_pts);
     launch(c, K_SORT, [&] {
       k_compact<D><<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(tabs[0].ent, p.slots, si.runs, &ctrl->nruns);
     });
+    check_launch();
+    return true;
   } else {
+    launch(c, K_SORT, [&] { k_hist<D, Tab, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
     GS_CUDA(cudaMemcpyAsync(si.runs, tabs[0].list, p.list_cap * sizeof(u32), cudaMemcpyDeviceToDevice, c->st));
     GS_CUDA(cudaMemcpyAsync(&ctrl->nruns, &ctrl->k[0], sizeof(u32), cudaMemcpyDeviceToDevice, c->st));
+    launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, p.slots); });
+    launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
+    launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, off, p.slots, si.start); });
+    double* stage = ensure<double>(c, c->stage, (size_t)n * StageRec<D>::W);
+    launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, stage, n, p.g, tabs[0], off, nullptr,
+                                                                              si.cell0, si.minidx, ctrl); });
+    launch(c, K_SORT, [&] { k_unstage<D><<<nb_pts, kThreads, 0, c->st>>>(stage, y1, n, p.g.ld); });
+    clear_table<D>(c, p, tabs[0], &ctrl->k[0]);
+    check_launch();
+    std::swap(c->y[0], c->y[1]);
+    return false;
   }
-  launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, p.slots); });
-  launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
-  launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, off, p.slots, si.start); });
-  double* stage = ensure<double>(c, c->stage, (size_t)n * StageRec<D>::W);
-  launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, stage, n, p.g, tabs[0], off, nullptr,
-                                                                            si.cell0, si.minidx, ctrl); });
-  launch(c, K_SORT, [&] { k_unstage<D><<<nb_pts, kThreads, 0, c->st>>>(stage, y1, n, p.g.ld); });
-  clear_table<D>(c, p, tabs[0], &ctrl->k[0]);
-  check_launch();
-  std::swap(c->y[0], c->y[1]);
-  return si;
 }
 
 struct RunOut {
@@ -589,8 +623,9 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   reset_ctrl(c);
   SortInfo sinfo;
   const bool sorted = n >= kSortMinPoints;
+  bool table0 = false;   // the sort already built the table of y_0
   if (sorted)
-    sinfo = p.dense ? spatial_sort<D>(c, p, tabs.dn, n) : spatial_sort<D>(c, p, tabs.hs, n);
+    table0 = p.dense ? spatial_sort<D>(c, p, tabs.dn, n, sinfo) : spatial_sort<D>(c, p, tabs.hs, n, sinfo);
   if (sorted && !p.dense) {
     // k never grows (k_{t+1} <= k_t: y_{t+1} takes at most k_t distinct
     // values), so the loop's hash tables only need 2*k_0 slots: compact
@@ -605,7 +640,9 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
       tabs = make_tabs<D>(c, p);
     }
   }
-  if (p.dense)
+  if (table0)
+    ;
+  else if (p.dense)
     enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
   else
     enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts);
@@ -891,8 +928,8 @@ void shard_plan_d(gs_ctx* c, ShardState* sh, const InitStats& s) {
   GS_CUDA(cudaMemsetAsync(ensure<u32>(c, c->k_hist, (size_t)sh->max_iters), 0, 4 * sh->max_iters, c->st));
   reset_ctrl(c);
   sh->sorted = sh->n >= kSortMinPoints;
-  if (sh->sorted) sh->si = spatial_sort<D>(c, p, tabs.dn, sh->n);
-  enqueue_first_hist<D>(c, p, tabs.dn, sh->n, nb_pts);
+  const bool table0 = sh->sorted && spatial_sort<D>(c, p, tabs.dn, sh->n, sh->si);
+  if (!table0) enqueue_first_hist<D>(c, p, tabs.dn, sh->n, nb_pts);
   check_launch();
 }
 
@@ -990,7 +1027,7 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
                  &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
-                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb};
+                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);

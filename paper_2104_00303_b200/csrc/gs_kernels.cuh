@@ -1163,17 +1163,22 @@ __device__ __forceinline__ u64 entry_count(const Entry<D>* ent, u32 s) { return 
 // *kp) or, for dense tables, every slot in key order (count nslots) -- the
 // latter makes the sorted point order the lexicographic cell order.
 __device__ __forceinline__ u32 scan_item(const u32* list, i64 a) { return list ? list[a] : (u32)a; }
+// counts come from the table entries, or from a plain u32 array (cnt32)
+template <int D>
+__device__ __forceinline__ u64 item_count(const Entry<D>* ent, const u32* cnt32, u32 s) {
+  return cnt32 ? (u64)cnt32[s] : ent[s].count;
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_scan_reduce(const Entry<D>* ent, const u32* list, const u32* kp,
-                                                          u64* bsum, u64 nslots) {
+                                                          u64* bsum, u64 nslots, const u32* cnt32 = nullptr) {
   const u64 k = list ? (u64)*kp : nslots;
   const i64 a0 = (i64)blockIdx.x * kScanChunk;
   u64 s = 0;
   if (a0 < k) {
     for (int it = 0; it < kScanItems; ++it) {
       const i64 a = a0 + (i64)it * kThreads + threadIdx.x;
-      if (a < (i64)k) s += entry_count<D>(ent, scan_item(list, a));
+      if (a < (i64)k) s += item_count<D>(ent, cnt32, scan_item(list, a));
     }
   }
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
@@ -1223,7 +1228,8 @@ __global__ void __launch_bounds__(1024) k_scan_top(u64* bsum, int nb) {
 // per-cell write cursor = exclusive prefix of counts (list order)
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, const u32* list, const u32* kp,
-                                                         const u64* bsum, u32* off, u64 nslots, u32* start) {
+                                                         const u64* bsum, u32* off, u64 nslots, u32* start,
+                                                         const u32* cnt32 = nullptr) {
   const u64 k = list ? (u64)*kp : nslots;
   const i64 a0 = (i64)blockIdx.x * kScanChunk;
   if (a0 >= (i64)k) return;
@@ -1232,7 +1238,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(const Entry<D>* ent, co
   u64 tot = 0;
   for (int it = 0; it < kScanItems; ++it) {
     const i64 a = a0 + (i64)threadIdx.x * kScanItems + it;
-    c[it] = a < (i64)k ? entry_count<D>(ent, scan_item(list, a)) : 0;
+    c[it] = a < (i64)k ? item_count<D>(ent, cnt32, scan_item(list, a)) : 0;
     tot += c[it];
   }
   u64 x = tot;
@@ -1365,6 +1371,330 @@ __global__ void __launch_bounds__(kThreads) k_labels_runs(const u32* __restrict_
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const u32 s0 = cell0[i];   // 0xffffffff only after a flagged lookup failure
     labels[i] = s0 == 0xffffffffu ? -1 : (i64)rankmap[runroot[s0]];
+  }
+}
+
+// ------------------------------------------- two-level sort (dense tables)
+// The one-time spatial sort without per-point global atomics:
+//   k_bk_count   per block chunk: shared-memory histogram of coarse buckets
+//                (2^shift consecutive slots), each point's slot -> cell0
+//   k_bk_cols    per bucket: exclusive scan over the blocks (in place)
+//   k_bk_stage   per block chunk, in rounds of kStageRound points: local
+//                counting sort by bucket in shared memory, then coalesced
+//                writes of bucket runs into the bucket-grouped staging buffer
+//   k_bk_tally   per fixed-size chunk of staging (load-balanced whatever the
+//                bucket sizes): shared-memory count / min index per slot,
+//                one global atomic pair per (chunk, slot) -> run sizes + minima
+//   (scan of the run sizes over slots -> run starts / cursors)
+//   k_bk_place   per chunk again: per-slot cursor bump once per (chunk, slot),
+//                warp-aggregated local ranks, SoA writes of the sorted iterate
+// Chunks whose slots span more than the shared-memory window fall back to
+// per-record global atomics (correct, just slower; never seen on the configs).
+template <int D>
+struct StRec {
+  static constexpr int W = ((D + 1) + 1) & ~1;   // D coords + (slot<<32 | index) + pad
+};
+constexpr int kChunkRecs = 4096;
+template <int D>
+constexpr int kTallyWin = (D <= 5) ? 2048 : 1024;
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_bk_count(const double* __restrict__ y, i64 n, GridParams g,
+                                                       int shift, u32 nb, i64 chunk, u32* blk_counts,
+                                                       u32* cell0, Ctrl* ctrl) {
+  extern __shared__ u32 hist[];
+  for (u32 b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const i64 a0 = (i64)blockIdx.x * chunk, a1 = min(n, a0 + chunk);
+  for (i64 base = a0; base < a1; base += blockDim.x) {
+    const i64 i = base + threadIdx.x;
+    u32 bk = 0xffffffffu;
+    if (i < a1) {
+      double v[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * g.ld + i);
+      bool inside;
+      const u64 key = pack_key<D>(g, v, inside);
+      if (!inside) {
+        atomicOr(&ctrl->error, kErrMissing);
+        cell0[i] = 0xffffffffu;
+      } else {
+        cell0[i] = (u32)key;
+        bk = (u32)(key >> shift);
+      }
+    }
+    const unsigned peers = __match_any_sync(kFull, bk);
+    if (bk != 0xffffffffu && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + bk, (u32)__popc(peers));
+  }
+  __syncthreads();
+  for (u32 b = threadIdx.x; b < nb; b += blockDim.x) blk_counts[(i64)blockIdx.x * nb + b] = hist[b];
+}
+
+// one block per bucket: exclusive scan over the blocks' counts (in place)
+__global__ void __launch_bounds__(1024) k_bk_cols(u32* blk_counts, u32 nblk, u32 nb, u64* bucket_tot) {
+  const u32 b = blockIdx.x;
+  __shared__ u32 w[32];
+  __shared__ u32 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = 0; base < nblk; base += 1024) {
+    const u32 k = base + threadIdx.x;
+    const u32 v = k < nblk ? blk_counts[(i64)k * nb + b] : 0;
+    u32 x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 yv = __shfl_up_sync(kFull, x, o);
+      if ((threadIdx.x & 31) >= o) x += yv;
+    }
+    if ((threadIdx.x & 31) == 31) w[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      u32 z = w[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 yv = __shfl_up_sync(kFull, z, o);
+        if ((int)threadIdx.x >= o) z += yv;
+      }
+      w[threadIdx.x] = z;
+    }
+    __syncthreads();
+    const u32 before = (threadIdx.x >= 32 ? w[(threadIdx.x >> 5) - 1] : 0) + x - v;
+    if (k < nblk) blk_counts[(i64)k * nb + b] = carry + before;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += before + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bucket_tot[b] = carry;
+}
+
+// block-wide exclusive scan of n32 counters in shared memory (in place into out)
+__device__ __forceinline__ void block_exclusive_scan(const u32* in, u32* out, u32 nitems, u32* warpsum) {
+  const u32 per = (nitems + blockDim.x - 1) / blockDim.x;
+  const u32 q0 = threadIdx.x * per;
+  u32 run = 0;
+  for (u32 t = 0; t < per; ++t) run += (q0 + t < nitems) ? in[q0 + t] : 0;
+  u32 x = run;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 yv = __shfl_up_sync(kFull, x, o);
+    if ((threadIdx.x & 31) >= o) x += yv;
+  }
+  if ((threadIdx.x & 31) == 31) warpsum[threadIdx.x >> 5] = x;
+  __syncthreads();
+  u32 pre = x - run;
+  for (u32 w = 0; w < (threadIdx.x >> 5); ++w) pre += warpsum[w];
+  for (u32 t = 0; t < per; ++t) {
+    if (q0 + t >= nitems) break;
+    const u32 c = in[q0 + t];
+    out[q0 + t] = pre;
+    pre += c;
+  }
+  __syncthreads();
+}
+
+template <int D>
+constexpr int kStageRound = (D <= 4) ? 2048 : 1024;
+
+template <int D>
+__host__ __device__ constexpr size_t bk_stage_smem(u32 nb) {
+  return (size_t)kStageRound<D> * (StRec<D>::W * 8 + 4) + (size_t)3 * nb * 4;
+}
+
+template <int D>
+__global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, i64 n, GridParams g, int shift,
+                                                  u32 nb, i64 chunk, const u32* blk_off, const u64* bucket_base,
+                                                  const u32* __restrict__ cell0, double* __restrict__ stage) {
+  constexpr int W = StRec<D>::W;
+  constexpr int R = kStageRound<D>;
+  constexpr int PER = R / 512;
+  extern __shared__ __align__(16) unsigned char raw[];
+  double* recs = reinterpret_cast<double*>(raw);                   // [R][W]
+  u32* rbk = reinterpret_cast<u32*>(recs + (size_t)R * W);         // [R] bucket of local record
+  u32* gcur = rbk + R;                                             // [nb] global cursor
+  u32* lcnt = gcur + nb;                                           // [nb] round counts
+  u32* lst = lcnt + nb;                                            // [nb] round starts
+  __shared__ u32 warpsum[32];
+  for (u32 b = threadIdx.x; b < nb; b += blockDim.x)
+    gcur[b] = (u32)bucket_base[b] + blk_off[(i64)blockIdx.x * nb + b];
+  for (int q = threadIdx.x; q < R; q += blockDim.x) rbk[q] = 0xffffffffu;
+  const i64 a0 = (i64)blockIdx.x * chunk, a1 = min(n, a0 + chunk);
+  for (i64 r0 = a0; r0 < a1; r0 += R) {
+    const int m = (int)min((i64)R, a1 - r0);
+    for (u32 b = threadIdx.x; b < nb; b += blockDim.x) lcnt[b] = 0;
+    __syncthreads();
+    // local ranks per bucket (warp-aggregated shared-memory atomics)
+    u32 mybk[PER], myrk[PER];
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int q = t * 512 + threadIdx.x;
+      const u32 key = q < m ? cell0[r0 + q] : 0xffffffffu;
+      const u32 bk = key == 0xffffffffu ? 0xffffffffu : key >> shift;
+      const unsigned peers = __match_any_sync(kFull, bk);
+      const int leader = __ffs(peers) - 1;
+      u32 base = 0;
+      if (bk != 0xffffffffu && (int)(threadIdx.x & 31) == leader) base = atomicAdd(lcnt + bk, (u32)__popc(peers));
+      base = __shfl_sync(kFull, base, leader);
+      mybk[t] = bk;
+      myrk[t] = base + __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+    }
+    __syncthreads();
+    block_exclusive_scan(lcnt, lst, nb, warpsum);
+    // records into bucket order in shared memory
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int q = t * 512 + threadIdx.x;
+      if (q >= m || mybk[t] == 0xffffffffu) continue;
+      const i64 i = r0 + q;
+      const u32 lpos = lst[mybk[t]] + myrk[t];
+      double* rec = recs + (size_t)lpos * W;
+#pragma unroll
+      for (int j = 0; j < D; ++j) rec[j] = __ldcs(y + (i64)j * g.ld + i);
+      rec[D] = __longlong_as_double((long long)(((u64)cell0[i] << 32) | (u64)(u32)i));
+#pragma unroll
+      for (int j = D + 1; j < W; ++j) rec[j] = 0.0;
+      rbk[lpos] = mybk[t];
+    }
+    __syncthreads();
+    // coalesced write-out: consecutive local records of one bucket go to
+    // consecutive staging records
+    for (int q = threadIdx.x; q < m; q += blockDim.x) {
+      const u32 bk = rbk[q];
+      if (bk == 0xffffffffu) continue;
+      const u32 pos = gcur[bk] + (q - lst[bk]);
+      const double2* src = reinterpret_cast<const double2*>(recs + (size_t)q * W);
+      double2* dst = reinterpret_cast<double2*>(stage + (i64)pos * W);
+#pragma unroll
+      for (int w = 0; w < W / 2; ++w) dst[w] = src[w];
+      rbk[q] = 0xffffffffu;
+    }
+    __syncthreads();
+    for (u32 b = threadIdx.x; b < nb; b += blockDim.x) gcur[b] += lcnt[b];
+    __syncthreads();
+  }
+}
+
+// slot range [kmin, kmax] of a staging chunk (block-wide)
+template <int D>
+__device__ __forceinline__ void chunk_range(const double* __restrict__ stage, i64 r0, i64 r1, u32* kmin_s,
+                                            u32* kmax_s) {
+  constexpr int W = StRec<D>::W;
+  if (threadIdx.x == 0) { *kmin_s = 0xffffffffu; *kmax_s = 0; }
+  __syncthreads();
+  u32 lmin = 0xffffffffu, lmax = 0;
+  for (i64 r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const u32 key = (u32)((u64)__double_as_longlong(stage[r * W + D]) >> 32);
+    lmin = min(lmin, key);
+    lmax = max(lmax, key);
+  }
+  lmin = __reduce_min_sync(kFull, lmin);
+  lmax = __reduce_max_sync(kFull, lmax);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(kmin_s, lmin);
+    atomicMax(kmax_s, lmax);
+  }
+  __syncthreads();
+}
+
+// per chunk of staging: per-slot counts and minimum original index through
+// shared-memory tallies over the chunk's slot window, then one global atomic
+// pair per (chunk, slot).  cnt must be zero on entry.
+template <int D>
+__global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ stage, i64 n, u64 nslots, u32* cnt,
+                                                  u32* minidx, Ctrl* ctrl) {
+  constexpr int W = StRec<D>::W;
+  constexpr int WIN = kTallyWin<D>;
+  __shared__ u32 lc[WIN], mn[WIN];
+  __shared__ u32 kmin_s, kmax_s;
+  const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
+  chunk_range<D>(stage, r0, r1, &kmin_s, &kmax_s);
+  const u32 kmin = kmin_s;
+  const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
+  const u32 span = wide ? 0 : kmax_s - kmin + 1;
+  for (u32 q = threadIdx.x; q < span; q += blockDim.x) {
+    lc[q] = 0;
+    mn[q] = 0xffffffffu;
+  }
+  __syncthreads();
+  for (i64 rb = r0; rb < r1; rb += blockDim.x) {
+    const i64 r = rb + threadIdx.x;
+    const bool valid = r < r1;
+    u32 key = 0xffffffffu, idx = 0xffffffffu;
+    if (valid) {
+      const u64 tag = (u64)__double_as_longlong(stage[r * W + D]);
+      key = (u32)(tag >> 32);
+      idx = (u32)tag;
+    }
+    if (wide) {
+      if (valid) {
+        if (key >= nslots) {
+          atomicOr(&ctrl->error, kErrMissing);
+        } else {
+          atomicAdd(cnt + key, 1u);
+          atomicMin(minidx + key, idx);
+        }
+      }
+      continue;
+    }
+    // lanes on one slot combine first (hot cells)
+    const unsigned peers = __match_any_sync(kFull, key);
+    const u32 mnv = __reduce_min_sync(peers, idx);
+    if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) {
+      atomicAdd(lc + (key - kmin), (u32)__popc(peers));
+      atomicMin(mn + (key - kmin), mnv);
+    }
+  }
+  __syncthreads();
+  for (u32 q = threadIdx.x; q < span; q += blockDim.x) {
+    if (!lc[q]) continue;
+    atomicAdd(cnt + kmin + q, lc[q]);
+    atomicMin(minidx + kmin + q, mn[q]);
+  }
+}
+
+// per chunk again: one global cursor bump per (chunk, slot), warp-aggregated
+// local ranks, SoA writes of the sorted iterate (off ends as run ends)
+template <int D>
+__global__ void __launch_bounds__(512) k_bk_place(const double* __restrict__ stage, i64 n, u64 nslots, GridParams g,
+                                                  u32* off, double* __restrict__ ys) {
+  constexpr int W = StRec<D>::W;
+  constexpr int WIN = kTallyWin<D>;
+  __shared__ u32 cnt[WIN];
+  __shared__ u32 kmin_s, kmax_s;
+  const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
+  chunk_range<D>(stage, r0, r1, &kmin_s, &kmax_s);
+  const u32 kmin = kmin_s;
+  const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
+  if (!wide) {
+    const u32 span = kmax_s - kmin + 1;
+    for (u32 q = threadIdx.x; q < span; q += blockDim.x) cnt[q] = 0;
+    __syncthreads();
+    for (i64 r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      const u32 key = (u32)((u64)__double_as_longlong(stage[r * W + D]) >> 32);
+      atomicAdd(cnt + (key - kmin), 1u);
+    }
+    __syncthreads();
+    for (u32 q = threadIdx.x; q < span; q += blockDim.x)
+      if (cnt[q]) cnt[q] = atomicAdd(off + kmin + q, cnt[q]);   // now the chunk's base
+    __syncthreads();
+  }
+  for (i64 rb = r0; rb < r1; rb += blockDim.x) {
+    const i64 r = rb + threadIdx.x;
+    bool valid = r < r1;
+    u32 key = 0xffffffffu;
+    const double* rec = stage + r * W;
+    if (valid) key = (u32)((u64)__double_as_longlong(rec[D]) >> 32);
+    u32 pos = 0;
+    if (wide) {
+      if (valid && key >= nslots) valid = false;
+      if (valid) pos = atomicAdd(off + key, 1u);
+    } else {
+      const unsigned peers = __match_any_sync(kFull, key);
+      const int leader = __ffs(peers) - 1;
+      u32 base = 0;
+      if (valid && (int)(threadIdx.x & 31) == leader) base = atomicAdd(cnt + (key - kmin), (u32)__popc(peers));
+      pos = __shfl_sync(kFull, base, leader) + __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+    }
+    if (valid && pos < (u32)n) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * g.ld + pos, rec[j]);
+    }
   }
 }
 
