@@ -544,7 +544,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si) 
   const u32* list = Tab::kDense ? nullptr : tabs[0].list;
   if constexpr (Tab::kDense) {
     // coarse buckets of 2^shift consecutive slots, at most 2048 of them
-    int shift = 10;
+    int shift = kBucketShiftMin;
     while ((p.slots >> shift) >= 2048) ++shift;
     const u32 nb = (u32)((p.slots + (1ull << shift) - 1) >> shift);
     const u32 nblk = (u32)c->sms * 8;
@@ -556,6 +556,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si) 
     static bool attr = false;
     if (!attr) {
       GS_CUDA(cudaFuncSetAttribute(k_bk_stage<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_stage_smem<D>(2048)));
+      GS_CUDA(cudaFuncSetAttribute(k_bk_tally<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTallyWin * 4));
       attr = true;
     }
     const int nch = (int)((n + kChunkRecs - 1) / kChunkRecs);
@@ -564,11 +565,11 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si) 
     launch(c, K_SORT, [&] { k_bk_cols<<<nb, 1024, 0, c->st>>>(bk, nblk, nb, btot); });
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(btot, (int)nb); });
     launch(c, K_SORT, [&] { k_bk_stage<D><<<nblk, 512, st_smem, c->st>>>(y0, n, p.g, shift, nb, chunk, bk, btot, si.cell0, stage); });
-    launch(c, K_SORT, [&] { k_bk_tally<D><<<nch, 512, 0, c->st>>>(stage, n, p.slots, off, si.minidx, ctrl); });
+    launch(c, K_SORT, [&] { k_bk_tally<D><<<nch, 512, 2 * kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, off, si.minidx, ctrl); });
     launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, p.slots, off); });
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
     launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, off, p.slots, si.start, off); });
-    launch(c, K_SORT, [&] { k_bk_place<D><<<nch, 512, 0, c->st>>>(stage, n, p.slots, p.g, off, y1); });
+    launch(c, K_SORT, [&] { k_bk_place<D><<<nch, 512, kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, y1); });
     std::swap(c->y[0], c->y[1]);
     // table 0 from the sorted iterate (runs are contiguous: cheap), then the
     // occupied-slot list of the runs

@@ -1395,8 +1395,23 @@ struct StRec {
   static constexpr int W = ((D + 1) + 1) & ~1;   // D coords + (slot<<32 | index) + pad
 };
 constexpr int kChunkRecs = 4096;
-template <int D>
-constexpr int kTallyWin = (D <= 5) ? 2048 : 1024;
+constexpr int kBucketShiftMin = 12;        // >= 4096 slots per coarse bucket
+constexpr int kTallyWin = 2 << kBucketShiftMin;   // a chunk spans <= 2 buckets when they are full
+
+// Shared-memory counter bump returning each lane's rank.  __match_any_sync
+// saturates the ADU pipe at one match per point, so: one atomic for a warp
+// whose lanes all hit the same counter (sorted inputs, hot cells), plain
+// per-lane shared atomics otherwise (random inputs rarely collide).
+__device__ __forceinline__ u32 smem_bump(u32* ctr, u32 key, bool valid) {
+  const int lane = threadIdx.x & 31;
+  const u32 k0 = __shfl_sync(kFull, key, 0);
+  if (__all_sync(kFull, valid && key == k0)) {
+    u32 b = 0;
+    if (lane == 0) b = atomicAdd(ctr + k0, 32u);
+    return __shfl_sync(kFull, b, 0) + lane;
+  }
+  return valid ? atomicAdd(ctr + key, 1u) : 0u;
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_bk_count(const double* __restrict__ y, i64 n, GridParams g,
@@ -1423,8 +1438,7 @@ __global__ void __launch_bounds__(kThreads) k_bk_count(const double* __restrict_
         bk = (u32)(key >> shift);
       }
     }
-    const unsigned peers = __match_any_sync(kFull, bk);
-    if (bk != 0xffffffffu && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + bk, (u32)__popc(peers));
+    smem_bump(hist, bk, bk != 0xffffffffu);
   }
   __syncthreads();
   for (u32 b = threadIdx.x; b < nb; b += blockDim.x) blk_counts[(i64)blockIdx.x * nb + b] = hist[b];
@@ -1519,20 +1533,22 @@ __global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, 
     const int m = (int)min((i64)R, a1 - r0);
     for (u32 b = threadIdx.x; b < nb; b += blockDim.x) lcnt[b] = 0;
     __syncthreads();
-    // local ranks per bucket (warp-aggregated shared-memory atomics)
-    u32 mybk[PER], myrk[PER];
+    // all global loads of the round first (memory-level parallelism), then
+    // local ranks per bucket
+    u32 mykey[PER], mybk[PER], myrk[PER];
+    double myv[PER][D];
 #pragma unroll
     for (int t = 0; t < PER; ++t) {
       const int q = t * 512 + threadIdx.x;
-      const u32 key = q < m ? cell0[r0 + q] : 0xffffffffu;
-      const u32 bk = key == 0xffffffffu ? 0xffffffffu : key >> shift;
-      const unsigned peers = __match_any_sync(kFull, bk);
-      const int leader = __ffs(peers) - 1;
-      u32 base = 0;
-      if (bk != 0xffffffffu && (int)(threadIdx.x & 31) == leader) base = atomicAdd(lcnt + bk, (u32)__popc(peers));
-      base = __shfl_sync(kFull, base, leader);
+      mykey[t] = q < m ? __ldcs(cell0 + r0 + q) : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < D; ++j) myv[t][j] = q < m ? __ldcs(y + (i64)j * g.ld + r0 + q) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const u32 bk = mykey[t] == 0xffffffffu ? 0xffffffffu : mykey[t] >> shift;
       mybk[t] = bk;
-      myrk[t] = base + __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+      myrk[t] = smem_bump(lcnt, bk, bk != 0xffffffffu);
     }
     __syncthreads();
     block_exclusive_scan(lcnt, lst, nb, warpsum);
@@ -1540,13 +1556,12 @@ __global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, 
 #pragma unroll
     for (int t = 0; t < PER; ++t) {
       const int q = t * 512 + threadIdx.x;
-      if (q >= m || mybk[t] == 0xffffffffu) continue;
-      const i64 i = r0 + q;
+      if (mybk[t] == 0xffffffffu) continue;
       const u32 lpos = lst[mybk[t]] + myrk[t];
       double* rec = recs + (size_t)lpos * W;
 #pragma unroll
-      for (int j = 0; j < D; ++j) rec[j] = __ldcs(y + (i64)j * g.ld + i);
-      rec[D] = __longlong_as_double((long long)(((u64)cell0[i] << 32) | (u64)(u32)i));
+      for (int j = 0; j < D; ++j) rec[j] = myv[t][j];
+      rec[D] = __longlong_as_double((long long)(((u64)mykey[t] << 32) | (u64)(u32)(r0 + q)));
 #pragma unroll
       for (int j = D + 1; j < W; ++j) rec[j] = 0.0;
       rbk[lpos] = mybk[t];
@@ -1570,16 +1585,30 @@ __global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, 
   }
 }
 
-// slot range [kmin, kmax] of a staging chunk (block-wide)
+// A chunk = kChunkRecs staging records, kRpt per thread of a 512-thread
+// block (record r0 + t*512 + tid); each thread keeps its records' tags
+// (slot << 32 | original index) in registers across the passes.
+constexpr int kRpt = kChunkRecs / 512;
+
 template <int D>
-__device__ __forceinline__ void chunk_range(const double* __restrict__ stage, i64 r0, i64 r1, u32* kmin_s,
-                                            u32* kmax_s) {
+__device__ __forceinline__ void load_tags(const double* __restrict__ stage, i64 r0, i64 r1, u64 (&tag)[kRpt]) {
   constexpr int W = StRec<D>::W;
+#pragma unroll
+  for (int t = 0; t < kRpt; ++t) {
+    const i64 r = r0 + t * 512 + threadIdx.x;
+    tag[t] = r < r1 ? (u64)__double_as_longlong(stage[r * W + D]) : ~0ull;
+  }
+}
+
+// slot range [kmin, kmax] of the chunk (block-wide)
+__device__ __forceinline__ void tags_range(const u64 (&tag)[kRpt], u32* kmin_s, u32* kmax_s) {
   if (threadIdx.x == 0) { *kmin_s = 0xffffffffu; *kmax_s = 0; }
   __syncthreads();
   u32 lmin = 0xffffffffu, lmax = 0;
-  for (i64 r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    const u32 key = (u32)((u64)__double_as_longlong(stage[r * W + D]) >> 32);
+#pragma unroll
+  for (int t = 0; t < kRpt; ++t) {
+    if (tag[t] == ~0ull) continue;
+    const u32 key = (u32)(tag[t] >> 32);
     lmin = min(lmin, key);
     lmax = max(lmax, key);
   }
@@ -1598,12 +1627,15 @@ __device__ __forceinline__ void chunk_range(const double* __restrict__ stage, i6
 template <int D>
 __global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ stage, i64 n, u64 nslots, u32* cnt,
                                                   u32* minidx, Ctrl* ctrl) {
-  constexpr int W = StRec<D>::W;
-  constexpr int WIN = kTallyWin<D>;
-  __shared__ u32 lc[WIN], mn[WIN];
+  constexpr int WIN = kTallyWin;
+  extern __shared__ u32 tsm[];
+  u32* lc = tsm;
+  u32* mn = tsm + WIN;
   __shared__ u32 kmin_s, kmax_s;
   const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
-  chunk_range<D>(stage, r0, r1, &kmin_s, &kmax_s);
+  u64 tag[kRpt];
+  load_tags<D>(stage, r0, r1, tag);
+  tags_range(tag, &kmin_s, &kmax_s);
   const u32 kmin = kmin_s;
   const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
   const u32 span = wide ? 0 : kmax_s - kmin + 1;
@@ -1612,15 +1644,10 @@ __global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ sta
     mn[q] = 0xffffffffu;
   }
   __syncthreads();
-  for (i64 rb = r0; rb < r1; rb += blockDim.x) {
-    const i64 r = rb + threadIdx.x;
-    const bool valid = r < r1;
-    u32 key = 0xffffffffu, idx = 0xffffffffu;
-    if (valid) {
-      const u64 tag = (u64)__double_as_longlong(stage[r * W + D]);
-      key = (u32)(tag >> 32);
-      idx = (u32)tag;
-    }
+#pragma unroll
+  for (int t = 0; t < kRpt; ++t) {
+    const bool valid = tag[t] != ~0ull;
+    const u32 key = (u32)(tag[t] >> 32), idx = (u32)tag[t];
     if (wide) {
       if (valid) {
         if (key >= nslots) {
@@ -1632,12 +1659,17 @@ __global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ sta
       }
       continue;
     }
-    // lanes on one slot combine first (hot cells)
-    const unsigned peers = __match_any_sync(kFull, key);
-    const u32 mnv = __reduce_min_sync(peers, idx);
-    if (valid && (int)(threadIdx.x & 31) == __ffs(peers) - 1) {
-      atomicAdd(lc + (key - kmin), (u32)__popc(peers));
-      atomicMin(mn + (key - kmin), mnv);
+    // one atomic pair for a warp on a single slot (hot cells), else per lane
+    const u32 k0 = __shfl_sync(kFull, key, 0);
+    if (__all_sync(kFull, valid && key == k0)) {
+      const u32 mnv = __reduce_min_sync(kFull, idx);
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(lc + (k0 - kmin), 32u);
+        atomicMin(mn + (k0 - kmin), mnv);
+      }
+    } else if (valid) {
+      atomicAdd(lc + (key - kmin), 1u);
+      atomicMin(mn + (key - kmin), idx);
     }
   }
   __syncthreads();
@@ -1648,53 +1680,49 @@ __global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ sta
   }
 }
 
-// per chunk again: one global cursor bump per (chunk, slot), warp-aggregated
+// per chunk again: one global cursor bump per (chunk, slot), shared-memory
 // local ranks, SoA writes of the sorted iterate (off ends as run ends)
 template <int D>
 __global__ void __launch_bounds__(512) k_bk_place(const double* __restrict__ stage, i64 n, u64 nslots, GridParams g,
                                                   u32* off, double* __restrict__ ys) {
   constexpr int W = StRec<D>::W;
-  constexpr int WIN = kTallyWin<D>;
-  __shared__ u32 cnt[WIN];
+  constexpr int WIN = kTallyWin;
+  extern __shared__ u32 cnt[];
   __shared__ u32 kmin_s, kmax_s;
   const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
-  chunk_range<D>(stage, r0, r1, &kmin_s, &kmax_s);
+  u64 tag[kRpt];
+  load_tags<D>(stage, r0, r1, tag);
+  tags_range(tag, &kmin_s, &kmax_s);
   const u32 kmin = kmin_s;
   const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
+  u32 pos[kRpt];
   if (!wide) {
     const u32 span = kmax_s - kmin + 1;
     for (u32 q = threadIdx.x; q < span; q += blockDim.x) cnt[q] = 0;
     __syncthreads();
-    for (i64 r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-      const u32 key = (u32)((u64)__double_as_longlong(stage[r * W + D]) >> 32);
-      atomicAdd(cnt + (key - kmin), 1u);
-    }
+#pragma unroll
+    for (int t = 0; t < kRpt; ++t) pos[t] = smem_bump(cnt, (u32)(tag[t] >> 32) - kmin, tag[t] != ~0ull);
     __syncthreads();
     for (u32 q = threadIdx.x; q < span; q += blockDim.x)
       if (cnt[q]) cnt[q] = atomicAdd(off + kmin + q, cnt[q]);   // now the chunk's base
     __syncthreads();
-  }
-  for (i64 rb = r0; rb < r1; rb += blockDim.x) {
-    const i64 r = rb + threadIdx.x;
-    bool valid = r < r1;
-    u32 key = 0xffffffffu;
-    const double* rec = stage + r * W;
-    if (valid) key = (u32)((u64)__double_as_longlong(rec[D]) >> 32);
-    u32 pos = 0;
-    if (wide) {
-      if (valid && key >= nslots) valid = false;
-      if (valid) pos = atomicAdd(off + key, 1u);
-    } else {
-      const unsigned peers = __match_any_sync(kFull, key);
-      const int leader = __ffs(peers) - 1;
-      u32 base = 0;
-      if (valid && (int)(threadIdx.x & 31) == leader) base = atomicAdd(cnt + (key - kmin), (u32)__popc(peers));
-      pos = __shfl_sync(kFull, base, leader) + __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
-    }
-    if (valid && pos < (u32)n) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * g.ld + pos, rec[j]);
+    for (int t = 0; t < kRpt; ++t)
+      if (tag[t] != ~0ull) pos[t] += cnt[(u32)(tag[t] >> 32) - kmin];
+  } else {
+#pragma unroll
+    for (int t = 0; t < kRpt; ++t) {
+      const u32 key = (u32)(tag[t] >> 32);
+      if (tag[t] != ~0ull && key >= nslots) tag[t] = ~0ull;
+      pos[t] = tag[t] != ~0ull ? atomicAdd(off + key, 1u) : 0u;
     }
+  }
+#pragma unroll
+  for (int t = 0; t < kRpt; ++t) {
+    if (tag[t] == ~0ull || pos[t] >= (u32)n) continue;
+    const double* rec = stage + (r0 + t * 512 + threadIdx.x) * W;
+#pragma unroll
+    for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * g.ld + pos[t], rec[j]);
   }
 }
 
