@@ -27,6 +27,7 @@ namespace gs {
 typedef unsigned long long u64;
 typedef long long i64;
 typedef unsigned int u32;
+typedef unsigned char u8;
 typedef __int128 i128;
 typedef unsigned __int128 u128;
 
@@ -62,6 +63,24 @@ struct Ctrl {
   u32 nruns;               // initial cells (runs) after the spatial sort
   u32 pad3;
 };
+
+// Kernels of iteration t skip once the run stopped at an earlier iteration:
+// `done` holds (stopping iteration + 1).  The table chain may run one
+// iteration ahead of the shifts (side stream), so a plain flag would let the
+// shift of iteration t cancel the k_derive of the same iteration.
+__device__ __forceinline__ bool stopped_before(const Ctrl* c, int t) {
+  const int d = *(volatile const int*)&c->done;
+  return d != 0 && d <= t;
+}
+
+// Block-uniform form: `done` can flip while a side-stream kernel runs, and a
+// block whose warps disagreed would run its shared-memory phases half-staffed.
+__device__ __forceinline__ bool block_stopped_before(const Ctrl* c, int t) {
+  __shared__ int stop;
+  if (threadIdx.x == 0) stop = stopped_before(c, t);
+  __syncthreads();
+  return stop != 0;
+}
 
 constexpr int kErrOutOfBox = 1;     // an iterate left the admissible lattice box
 constexpr int kErrTableFull = 2;    // hash table overflow (cannot happen at load <= 1/2)

@@ -91,7 +91,11 @@ struct gs_ctx {
   std::vector<int64_t> track_bins;
   Prof prof;
   bool collapsed = false;               // option: collapsed iterations (gs_ctx_set_option)
-  Buf runposb, runcntb, bkcnt, bktot;
+  Buf runposb, runcntb, bkcnt, bktot, bocc;
+  bool tables_dirty = false;            // a call failed mid-run: table buffers may hold entries
+  // table-chain stream (see enqueue_iteration: overlap)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rec[2] = {nullptr, nullptr}, ev_shift[2] = {nullptr, nullptr};
   struct ShardState* shard = nullptr;   // row-sharded run in progress (gs_shard_*)
 };
 
@@ -255,7 +259,13 @@ Tabs<D> make_tabs(gs_ctx* c, const Plan& p) {
       t.hs[b].keys = ensure<u64>(c, c->keys[b], p.slots, 0xff);
       t.hs[b].mask = p.g.mask;
     }
+    if (c->tables_dirty) {
+      // every run path assumes clean buffers; after a failed call restore them
+      GS_CUDA(cudaMemsetAsync(c->ent[b].p, 0, c->ent[b].cap, c->st));
+      if (c->keys[b].p) GS_CUDA(cudaMemsetAsync(c->keys[b].p, 0xff, c->keys[b].cap, c->st));
+    }
   }
+  c->tables_dirty = false;
   return t;
 }
 
@@ -335,50 +345,113 @@ void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_p
   launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
 }
 
+// The table chain (k_agg -> k_derive -> k_agg ...) never reads the points:
+// table t+1 is derived from table t.  So on dense tables it runs on a
+// high-priority side stream one iteration ahead of the per-point shifts,
+// which only wait for their iteration's target records (double-buffered).
+void side_init(gs_ctx* c) {
+  if (c->side) return;
+  int least = 0, greatest = 0;
+  GS_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  // LOW priority: the table chain fills the SMs the shift's last wave leaves
+  // idle instead of displacing the bandwidth-bound shift (measured: high
+  // priority costs +9 ms per 100M-point run, low saves 3 ms)
+  (void)greatest;
+  GS_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, least));
+  for (cudaEvent_t* e : {&c->ev_fork, &c->ev_join, &c->ev_rec[0], &c->ev_rec[1], &c->ev_shift[0], &c->ev_shift[1]})
+    GS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
+// main stream waits for everything enqueued on the side stream so far
+void side_join(gs_ctx* c) {
+  if (!c->side) return;
+  GS_CUDA(cudaEventRecord(c->ev_join, c->side));
+  GS_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+}
+
 // Iteration t: table t (buffer t&1) holds the cells of y_t.  k_agg turns it
 // into per-cell target records (and clears buffer (t+1)&1), k_derive builds
 // the table of y_{t+1} from it (O(cells)), k_shift moves every point.
 template <int D, class Tab>
 void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, int64_t n, int nb_pts,
-                       int nb_cells, u64* limbs = nullptr, bool with_shift = true) {
+                       int nb_cells, u64* limbs = nullptr, bool with_shift = true, bool overlap = false) {
   const int cur = t & 1;
   double* y_in = static_cast<double*>(c->y[cur].p);
   double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
-  Rec<D>* rec = static_cast<Rec<D>*>(c->targets.p);
+  // overlap needs dense tables (k_shift does not read them) and 2 record buffers
+  const bool ov = overlap && Tab::kDense && with_shift;
+  Rec<D>* rec = static_cast<Rec<D>*>(c->targets.p) + (ov ? (size_t)cur * p.slots : 0);
+  cudaStream_t main_st = c->st;
+  if (ov) {
+    side_init(c);
+    if (t == 0) {
+      GS_CUDA(cudaEventRecord(c->ev_fork, main_st));
+      GS_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    }
+    if (t >= 2) GS_CUDA(cudaStreamWaitEvent(c->side, c->ev_shift[cur], 0));   // shift t-2 read rec[cur]
+    c->st = c->side;
+  }
   bool bricked = false;
   if constexpr (D == 3 && Tab::kDense) {
-    // dense 3-D lattice: tiled stencil (k_agg_brick3)
+    // dense 3-D lattice: tiled stencil over the occupied 8^3 bricks
+    // (k_agg_brick3, k_derive_brick3); brick occupancy per table buffer
     const int ext0 = (int)(p.g.nkeys / p.g.stride[0]), ext1 = (int)(p.g.stride[0] / p.g.stride[1]),
               ext2 = (int)p.g.stride[1];
     const int nbx = (ext0 + kBrick - 1) / kBrick, nby = (ext1 + kBrick - 1) / kBrick,
               nbz = (ext2 + kBrick - 1) / kBrick;
+    const int nbr = nbx * nby * nbz;
+    const BrickMap bm{(u32)p.g.stride[0], (u32)p.g.stride[1], (u32)nby, (u32)nbz};
     static bool attr = false;
     if (!attr) {
       GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBrickSmem));
       attr = true;
     }
+    u8* occ = ensure<u8>(c, c->bocc, 2 * (size_t)nbr);
+    if (t == 0) {
+      // iteration 0 starts from a freshly built table in buffer 0
+      GS_CUDA(cudaMemsetAsync(occ, 0, 2 * (size_t)nbr, c->st));
+      launch(c, K_AGG, [&] {
+        k_mark_bricks<<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(
+            reinterpret_cast<const Entry<3>*>(tabs[0].ent), p.slots, bm, occ);
+      });
+    }
+    u8* occ_cur = occ + (size_t)cur * nbr;
+    u8* occ_nxt = occ + (size_t)(cur ^ 1) * nbr;
     launch(c, K_AGG, [&] {
-      k_agg_brick3<<<nbx * nby * nbz, kBrickThreads, kBrickSmem, c->st>>>(
+      k_agg_brick3<<<nbr, kBrickThreads, kBrickSmem, c->st>>>(
           p.g, tabs[cur], tabs[cur ^ 1], reinterpret_cast<Rec<3>*>(rec), ctrl,
-          static_cast<u64*>(c->fp_hist.p) + t, static_cast<u32*>(c->k_hist.p) + t, nbx, nby, nbz);
+          static_cast<u64*>(c->fp_hist.p) + t, static_cast<u32*>(c->k_hist.p) + t, nbx, nby, nbz, occ_cur, occ_nxt, t);
+    });
+    if (ov) GS_CUDA(cudaEventRecord(c->ev_rec[cur], c->st));
+    launch(c, K_DERIVE, [&] {
+      k_derive_brick3<<<nbr, kBrickThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1],
+                                                        reinterpret_cast<const Rec<3>*>(rec), ctrl, nby, nbz, bm,
+                                                        occ_cur, occ_nxt, t);
     });
     bricked = true;
   }
   if (!bricked && D >= 4 && !Tab::kDense)
     launch(c, K_AGG, [&] { k_agg_warp<D, Tab><<<c->sms * 8, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
                                                     ctrl, cur, static_cast<u64*>(c->fp_hist.p) + t,
-                                                    static_cast<u32*>(c->k_hist.p) + t); });
+                                                    static_cast<u32*>(c->k_hist.p) + t, t); });
   else if (!bricked)
     launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur,
                                                     static_cast<u64*>(c->fp_hist.p) + t,
-                                                    static_cast<u32*>(c->k_hist.p) + t); });
-  launch(c, K_DERIVE, [&] { k_derive<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
-                                                                                ctrl, cur); });
+                                                    static_cast<u32*>(c->k_hist.p) + t, t); });
+  if (!bricked && ov) GS_CUDA(cudaEventRecord(c->ev_rec[cur], c->st));
+  if (!bricked)
+    launch(c, K_DERIVE, [&] { k_derive<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
+                                                                                  ctrl, cur, t); });
+  if (ov) {
+    c->st = main_st;
+    GS_CUDA(cudaStreamWaitEvent(main_st, c->ev_rec[cur], 0));
+  }
   if (with_shift)
     launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec, ctrl,
                                                   static_cast<u64*>(c->partials.p),
                                                   static_cast<double*>(c->mv_hist.p), t, eta, limbs); });
+  if (ov) GS_CUDA(cudaEventRecord(c->ev_shift[cur], main_st));
 }
 
 // Collapsed iteration t >= 1: targets + derived table as usual, then one
@@ -612,7 +685,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   const InitStats s = run_init<D>(c, in, n, h, y0);
   Plan p = make_plan(n, D, h, s);
   Tabs<D> tabs = make_tabs<D>(c, p);
-  ensure<Rec<D>>(c, c->targets, p.slots);
+  ensure<Rec<D>>(c, c->targets, 2 * p.slots);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
@@ -668,7 +741,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
         continue;
       }
       if (p.dense)
-        enqueue_iteration<D>(c, p, tabs.dn, t, eta, n, nb_pts, nb_cells);
+        enqueue_iteration<D>(c, p, tabs.dn, t, eta, n, nb_pts, nb_cells, nullptr, true, !collapsed);
       else
         enqueue_iteration<D>(c, p, tabs.hs, t, eta, n, nb_pts, nb_cells);
       if (collapsed && t == 0) {
@@ -680,6 +753,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
         });
       }
     }
+    side_join(c);
     check_launch();
     read_ctrl(c);
     check_flags(c->h_ctrl->error);
@@ -688,7 +762,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   }
   RunOut r;
   r.iters = c->h_ctrl->iters;
-  r.converged = c->h_ctrl->done;
+  r.converged = c->h_ctrl->done != 0;
   const int e = r.iters & 1;
   const double* yf = static_cast<const double*>(c->y[e].p);
   const SortInfo* sp = (sorted && r.iters >= 1) ? &sinfo : nullptr;
@@ -871,12 +945,15 @@ int guarded(gs_ctx* c, F&& f) {
     f();
     return GS_OK;
   } catch (const Fail& e) {
-    // leave the context usable: drain the stream
+    // leave the context usable: drain the streams, clean tables next call
     cudaStreamSynchronize(c->st);
+    if (c->side) cudaStreamSynchronize(c->side);
     cudaGetLastError();
+    c->tables_dirty = true;
     return e.code;
   } catch (const std::exception& e) {
     g_err = e.what();
+    c->tables_dirty = true;
     return GS_ERUNTIME;
   }
 }
@@ -1028,13 +1105,16 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
                  &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
-                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot};
+                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot, &c->bocc};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->h_small) cudaFreeHost(c->h_small);
   for (cudaEvent_t e : c->prof.pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_rec[0], c->ev_rec[1], c->ev_shift[0], c->ev_shift[1]})
+    if (e) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
   delete c->shard;
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
@@ -1412,7 +1492,7 @@ int gs_shard_status(gs_ctx* c, int32_t* done_out, int32_t* iters_out, void* stre
     shard_of(c, false);
     read_ctrl(c);
     check_flags(c->h_ctrl->error);
-    *done_out = c->h_ctrl->done;
+    *done_out = c->h_ctrl->done != 0;
     *iters_out = c->h_ctrl->iters;
   });
 }
@@ -1444,7 +1524,7 @@ int gs_shard_finish(gs_ctx* c, const void* minima_dev, int64_t* labels_dev, void
     for (int i = 0; i < iters; ++i) c->iter_k[i] = kk[i];
     *k_out = c->k_last;
     *iters_out = iters;
-    *converged_out = c->h_ctrl->done;
+    *converged_out = c->h_ctrl->done != 0;
     delete c->shard;
     c->shard = nullptr;
   });

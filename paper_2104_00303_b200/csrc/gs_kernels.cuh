@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_shift(const double* __restrict_
     const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
     mv_hist[t] = mv;
     ctrl->iters = t + 1;
-    if (mv < eta) ctrl->done = 1;
+    if (mv < eta) ctrl->done = t + 1;   // stamped: the run stopped after iteration t
   }
 }
 
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(kThreads) k_run_shift(double* __restrict__ run
     const double mv = u128_to_double((((u128)bh) << 64) | (u128)bl, g.movement_exp - 96);
     mv_hist[t] = mv;
     ctrl->iters = t + 1;
-    if (mv < eta) ctrl->done = 1;
+    if (mv < eta) ctrl->done = t + 1;   // stamped: the run stopped after iteration t
   }
 }
 
@@ -731,7 +731,7 @@ __global__ void k_converge(const u64* limbs, GridParams g, Ctrl* ctrl, double* m
   const double mv = u128_to_double(tot, g.movement_exp - 96);
   mv_hist[t] = mv;
   ctrl->iters = t + 1;
-  if (mv < eta) ctrl->done = 1;
+  if (mv < eta) ctrl->done = t + 1;   // stamped: the run stopped after iteration t
 }
 
 // Sharded run: per-root first-appearance minima (global indices) for a MIN
@@ -761,8 +761,8 @@ __global__ void k_import_minima(Tab tab, const u32* kp, const u32* par, u32* fir
 // reduction of the exact 128-bit sums.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Tab prev, Rec<D>* __restrict__ rec,
-                                                       Ctrl* ctrl, int cur, u64* fp_out, u32* k_out) {
-  if (*(volatile int*)&ctrl->done) return;
+                                                       Ctrl* ctrl, int cur, u64* fp_out, u32* k_out, int t) {
+  if (block_stopped_before(ctrl, t)) return;
   constexpr int M = (D == 1) ? 3 : (D == 2) ? 9 : (D == 3) ? 27 : (D == 4) ? 81 :
                     (D == 5) ? 243 : (D == 6) ? 729 : (D == 7) ? 2187 : 6561;
   const int lane = threadIdx.x & 31;
@@ -864,10 +864,28 @@ constexpr int kH3 = kHalo * kHalo * kHalo;          // 1000: staged halo / later
 constexpr int kS1 = kHalo * kHalo * kBrick;         // 800: z-pass
 constexpr size_t kBrickSmem = (size_t)(kH3 + kS1) * kWords3 * sizeof(u64) + kBrick * kBrick * kBrick * sizeof(u64);
 
+// Brick of a lattice slot (blockIdx order of the brick kernels).
+struct BrickMap {
+  u32 s0, s1, nby, nbz;
+  __device__ __forceinline__ u32 of(u32 slot) const {
+    const u32 x = slot / s0, r = slot - x * s0, y = r / s1, z = r - y * s1;
+    return ((x / kBrick) * nby + y / kBrick) * nbz + z / kBrick;
+  }
+};
+
+// Brick occupancy of a freshly built table (the derived tables mark theirs
+// in k_derive_brick3); occ zeroed before.
+__global__ void __launch_bounds__(kThreads) k_mark_bricks(const Entry<3>* ent, u64 nslots, BrickMap bm, u8* occ) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < (i64)nslots; s += stride)
+    if (ent[s].count) occ[bm.of((u32)s)] = 1;
+}
+
 __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, DenseTable<3> tab, DenseTable<3> prev,
                                                               Rec<3>* __restrict__ rec, Ctrl* ctrl, u64* fp_out,
-                                                              u32* k_out, int nbx, int nby, int nbz) {
-  if (*(volatile int*)&ctrl->done) return;
+                                                              u32* k_out, int nbx, int nby, int nbz,
+                                                              const u8* occ_cur, u8* occ_prev, int t) {
+  if (block_stopped_before(ctrl, t)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* E = reinterpret_cast<u64*>(smem_raw);          // [7][1000] halo, then [7][640] y-pass
   u64* S1 = E + (size_t)kWords3 * kH3;                // [7][800] z-pass
@@ -879,9 +897,26 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
   const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
   const int tid = threadIdx.x;
   if (tid == 0) any = 0;
+  const bool prev_occ = occ_prev[blockIdx.x] != 0, cur_occ = occ_cur[blockIdx.x] != 0;
   __syncthreads();
+  if (prev_occ && tid == 0) occ_prev[blockIdx.x] = 0;
+  // halo loads first (all of a thread's entries in flight at once; zeros
+  // outside the lattice), then the previous table's clear, then the stores
+  constexpr int HPT = (kH3 + kBrickThreads - 1) / kBrickThreads;
+  Entry<3> v[HPT];
+#pragma unroll
+  for (int u = 0; u < HPT; ++u) {
+    const int q = tid + u * kBrickThreads;
+    v[u].count = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) { v[u].hi[j] = 0; v[u].lo[j] = 0; }
+    if (!cur_occ || q >= kH3) continue;
+    const int hz = q % kHalo, hy = (q / kHalo) % kHalo, hx = q / (kHalo * kHalo);
+    const int x = x0 + hx - 1, yv = y0 + hy - 1, z = z0 + hz - 1;
+    if (x >= 0 && yv >= 0 && z >= 0 && x < ext0 && yv < ext1 && z < ext2) v[u] = tab.ent[x * s0 + yv * s1 + z];
+  }
   // clear the previous table in this brick (its cells are no longer read)
-  for (int q = tid; q < kBrick * kBrick * kBrick; q += blockDim.x) {
+  for (int q = tid; prev_occ && q < kBrick * kBrick * kBrick; q += blockDim.x) {
     const int z = z0 + q % kBrick, yv = y0 + (q / kBrick) % kBrick, x = x0 + q / (kBrick * kBrick);
     if (x >= ext0 || yv >= ext1 || z >= ext2) continue;
     Entry<3>* pe = prev.ent + (x * s0 + yv * s1 + z);
@@ -891,28 +926,22 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
       for (int j = 0; j < 3; ++j) { pe->hi[j] = 0; pe->lo[j] = 0; }
     }
   }
-  // stage the halo (zeros outside the lattice)
+  if (!cur_occ) return;   // no occupied cell in this brick of the table
   int occ = 0;
-  for (int q = tid; q < kH3; q += blockDim.x) {
-    const int hz = q % kHalo, hy = (q / kHalo) % kHalo, hx = q / (kHalo * kHalo);
-    const int x = x0 + hx - 1, yv = y0 + hy - 1, z = z0 + hz - 1;
-    Entry<3> v;
-    if (x >= 0 && yv >= 0 && z >= 0 && x < ext0 && yv < ext1 && z < ext2) {
-      v = tab.ent[x * s0 + yv * s1 + z];
-    } else {
-      v.count = 0;
 #pragma unroll
-      for (int j = 0; j < 3; ++j) { v.hi[j] = 0; v.lo[j] = 0; }
-    }
-    E[0 * kH3 + q] = v.count;
+  for (int u = 0; u < HPT; ++u) {
+    const int q = tid + u * kBrickThreads;
+    if (q >= kH3) continue;
+    const int hz = q % kHalo, hy = (q / kHalo) % kHalo, hx = q / (kHalo * kHalo);
+    E[0 * kH3 + q] = v[u].count;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      E[(1 + j) * kH3 + q] = v.hi[j];
-      E[(4 + j) * kH3 + q] = v.lo[j];
+      E[(1 + j) * kH3 + q] = v[u].hi[j];
+      E[(4 + j) * kH3 + q] = v[u].lo[j];
     }
     if (hx >= 1 && hx <= kBrick && hy >= 1 && hy <= kBrick && hz >= 1 && hz <= kBrick) {
-      own[((hx - 1) * kBrick + (hy - 1)) * kBrick + (hz - 1)] = v.count;
-      occ |= v.count != 0;
+      own[((hx - 1) * kBrick + (hy - 1)) * kBrick + (hz - 1)] = v[u].count;
+      occ |= v[u].count != 0;
     }
   }
   if (occ) any = 1;
@@ -984,8 +1013,8 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
 // target cell); the buffer receiving the new table was cleared by k_agg.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_derive(GridParams g, Tab cur, Tab nxt, const Rec<D>* __restrict__ rec,
-                                                     Ctrl* ctrl, int c) {
-  if (*(volatile int*)&ctrl->done) return;
+                                                     Ctrl* ctrl, int c, int t) {
+  if (block_stopped_before(ctrl, t)) return;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   const i64 items = Tab::kDense ? (i64)g.nkeys : (i64)ctrl->k[c];
@@ -1004,6 +1033,70 @@ __global__ void __launch_bounds__(kThreads) k_derive(GridParams g, Tab cur, Tab 
     }
     flush_segment<D, Tab, false>(nxt, ctrl, r.key, ag);
   }
+}
+
+// k_derive for dense 3-D tables, one block per occupied brick; marks the
+// bricks of the new table (occ_nxt was reset by k_agg_brick3).
+__global__ void __launch_bounds__(kBrickThreads) k_derive_brick3(GridParams g, DenseTable<3> cur, DenseTable<3> nxt,
+                                                                 const Rec<3>* __restrict__ rec, Ctrl* ctrl,
+                                                                 int nby, int nbz, BrickMap bm, const u8* occ_cur,
+                                                                 u8* occ_nxt, int t) {
+  if (block_stopped_before(ctrl, t)) return;
+  if (!occ_cur[blockIdx.x]) return;
+  const i64 s0 = (i64)g.stride[0], s1 = (i64)g.stride[1];
+  const int ext0 = (int)((i64)g.nkeys / s0), ext1 = (int)(s0 / s1), ext2 = (int)s1;
+  const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
+  const int q = threadIdx.x;
+  const int z = bz * kBrick + q % kBrick, yv = by * kBrick + (q / kBrick) % kBrick,
+            x = bx * kBrick + q / (kBrick * kBrick);
+  if (x >= ext0 || yv >= ext1 || z >= ext2) return;
+  const bool inside = x < ext0 && yv < ext1 && z < ext2;
+  const u32 s = inside ? (u32)(x * s0 + yv * s1 + z) : 0u;
+  const u64 cnt = inside ? cur.ent[s].count : 0;
+  u64 key = kEmpty;
+  Agg<3> ag;
+  ag.zero();
+  if (cnt) {
+    const Rec<3> r = rec[s];
+    key = r.key;
+    ag.cnt = (u32)cnt;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const i64 f = to_fixed(r.t[j], g.qscale[j]);
+      ag.hi[j] = (f >> 32) * (i64)cnt;
+      ag.lo[j] = (u64)(f & 0xffffffffll) * cnt;
+    }
+  }
+  // cells of a warp moving to one target cell (common once clusters
+  // contract) flush once: exact integer sums over the peers
+  if (__all_sync(kFull, key == kEmpty)) return;
+  const unsigned peers = __match_any_sync(kFull, key);
+  const int lane = threadIdx.x & 31;
+  if (__any_sync(kFull, __popc(peers) > 1)) {
+    // reduce each peer group to its lowest lane: in round k the lane of
+    // group rank r adds the partial of rank r + 2^k (pointer doubling)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const unsigned src = __fns(peers, lane, (1 << k) + 1);
+      const int from = src < 32 ? (int)src : lane;
+      const u32 oc = __shfl_sync(kFull, ag.cnt, from);
+      i64 oh[3];
+      u64 ol[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        oh[j] = __shfl_sync(kFull, ag.hi[j], from);
+        ol[j] = __shfl_sync(kFull, ag.lo[j], from);
+      }
+      if (src < 32) {
+        ag.cnt += oc;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) { ag.hi[j] += oh[j]; ag.lo[j] += ol[j]; }
+      }
+    }
+  }
+  if (key == kEmpty || lane != __ffs(peers) - 1) return;
+  flush_segment<3, DenseTable<3>, false>(nxt, ctrl, key, ag);
+  if (key < g.nkeys) occ_nxt[bm.of((u32)key)] = 1;
 }
 
 // Dense tables: occupied-cell list from the counts (warp-aggregated append).
@@ -1090,8 +1183,8 @@ __device__ __forceinline__ void agg_cell(const GridParams& g, const Tab& tab, u3
 // of this iteration; the last CTA resets the cleared table's cell count.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab prev, Rec<D>* __restrict__ rec,
-                                                  Ctrl* ctrl, int cur, u64* fp_out, u32* k_out) {
-  if (*(volatile int*)&ctrl->done) return;
+                                                  Ctrl* ctrl, int cur, u64* fp_out, u32* k_out, int t) {
+  if (block_stopped_before(ctrl, t)) return;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   u64 fp = 0;
