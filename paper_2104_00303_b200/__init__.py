@@ -7,6 +7,7 @@ Importing this package does not load the library; the first engine call
 does, and raises if it is missing -- there is no CPU fallback.
 """
 
+from .batch import segment_batch
 from .grid import (CellTables, PointSet, bin_point, bin_points, build_cell_tables,
                    neighbor_aggregate, neighbor_stats)
 from .modeseek import (ENGINES, Labeling, ShiftConfig, ShiftTrace, extract_clusters, install,
@@ -20,6 +21,6 @@ __all__ = [
     "ShiftConfig", "ShiftTrace", "TrackState", "Window", "bin_point", "bin_points",
     "build_cell_tables", "cluster_window", "extract_clusters", "image_to_features",
     "init_tracker", "install", "meanshiftpp", "meanshiftpp_device", "meanshiftpp_points", "meanshiftpp_step",
-    "neighbor_aggregate", "neighbor_stats", "neighborhood", "segment_image", "segment_pixels",
+    "neighbor_aggregate", "neighbor_stats", "neighborhood", "segment_batch", "segment_image", "segment_pixels",
     "track_frame", "track_sequence",
 ]
