@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #ifndef GS_MAXD
@@ -102,6 +103,19 @@ __host__ __device__ inline u64 mix64(u64 z) {
   return z ^ (z >> 31);
 }
 
+// x * 2^k, rounded once like ldexp: a multiply by the power of two when
+// 2^k is a normal double (IEEE multiply rounds exactly as ldexp does), the
+// library ldexp otherwise.
+__host__ __device__ inline double scale2(double x, int k) {
+  if (k >= -1022 && k <= 1023) {
+    u64 bits = (u64)(k + 1023) << 52;
+    double p;
+    memcpy(&p, &bits, sizeof p);
+    return x * p;
+  }
+  return ldexp(x, k);
+}
+
 // Correctly rounded (round-to-nearest-even) value of v * 2^e as a double.
 __host__ __device__ inline double i128_to_double(i128 v, int e) {
   if (v == 0) return 0.0;
@@ -129,7 +143,7 @@ __host__ __device__ inline double i128_to_double(i128 v, int e) {
       if (m == (1ull << 53)) { m >>= 1; sh += 1; }
     }
   }
-  double r = ldexp((double)m, e + sh);
+  double r = scale2((double)m, e + sh);
   return neg ? -r : r;
 }
 
@@ -147,11 +161,11 @@ __device__ __forceinline__ i64 to_fixed(double y, double qscale) {
 // 128-bit fixed-point image of a non-negative norm: rne(m * 2^(96-E)).
 __device__ __forceinline__ u128 norm_to_fixed(double m, int movement_exp) {
   // split at 2^48 so both halves convert exactly
-  const double a = ldexp(m, 48 - movement_exp);     // < 2^48
+  const double a = scale2(m, 48 - movement_exp);     // < 2^48
   const double ia = floor(a);
   const double r = __dsub_rn(a, ia);               // exact
   const u64 hi = (u64)ia;
-  const u64 lo = (u64)__double2ll_rn(ldexp(r, 48));
+  const u64 lo = (u64)__double2ll_rn(scale2(r, 48));
   return (((u128)hi) << 48) + (u128)lo;
 }
 

@@ -91,7 +91,7 @@ struct gs_ctx {
   std::vector<int64_t> track_bins;
   Prof prof;
   bool collapsed = false;               // option: collapsed iterations (gs_ctx_set_option)
-  Buf runposb, runcntb, bkcnt, bktot, bocc;
+  Buf runposb, runcntb, bkcnt, bktot, bocc, bmask;
   bool tables_dirty = false;            // a call failed mid-run: table buffers may hold entries
   // table-chain stream (see enqueue_iteration: overlap)
   cudaStream_t side = nullptr;
@@ -408,9 +408,11 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
       attr = true;
     }
     u8* occ = ensure<u8>(c, c->bocc, 2 * (size_t)nbr);
+    u32* mask = ensure<u32>(c, c->bmask, 2 * (size_t)nbr * 16);
     if (t == 0) {
       // iteration 0 starts from a freshly built table in buffer 0
       GS_CUDA(cudaMemsetAsync(occ, 0, 2 * (size_t)nbr, c->st));
+      GS_CUDA(cudaMemsetAsync(mask, 0, 2 * (size_t)nbr * 16 * sizeof(u32), c->st));
       launch(c, K_AGG, [&] {
         k_mark_bricks<<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(
             reinterpret_cast<const Entry<3>*>(tabs[0].ent), p.slots, bm, occ);
@@ -421,7 +423,8 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     launch(c, K_AGG, [&] {
       k_agg_brick3<<<nbr, kBrickThreads, kBrickSmem, c->st>>>(
           p.g, tabs[cur], tabs[cur ^ 1], reinterpret_cast<Rec<3>*>(rec), ctrl,
-          static_cast<u64*>(c->fp_hist.p) + t, static_cast<u32*>(c->k_hist.p) + t, nbx, nby, nbz, occ_cur, occ_nxt, t);
+          static_cast<u64*>(c->fp_hist.p) + t, static_cast<u32*>(c->k_hist.p) + t, nbx, nby, nbz, occ_cur, occ_nxt,
+          mask + (size_t)(cur ^ 1) * nbr * 16, mask + (size_t)cur * nbr * 16, t);
     });
     if (ov) GS_CUDA(cudaEventRecord(c->ev_rec[cur], c->st));
     launch(c, K_DERIVE, [&] {
@@ -1105,7 +1108,7 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
                  &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
-                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot, &c->bocc};
+                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot, &c->bocc, &c->bmask};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);

@@ -859,6 +859,7 @@ __global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Ta
 constexpr int kBrick = 8;
 constexpr int kHalo = kBrick + 2;
 constexpr int kBrickThreads = 512;
+static_assert(kBrickThreads == kBrick * kBrick * kBrick, "one thread per brick cell (occupancy ballots)");
 constexpr int kWords3 = 7;   // count, hi[3], lo[3]
 constexpr int kH3 = kHalo * kHalo * kHalo;          // 1000: staged halo / later the y-pass
 constexpr int kS1 = kHalo * kHalo * kBrick;         // 800: z-pass
@@ -884,7 +885,8 @@ __global__ void __launch_bounds__(kThreads) k_mark_bricks(const Entry<3>* ent, u
 __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, DenseTable<3> tab, DenseTable<3> prev,
                                                               Rec<3>* __restrict__ rec, Ctrl* ctrl, u64* fp_out,
                                                               u32* k_out, int nbx, int nby, int nbz,
-                                                              const u8* occ_cur, u8* occ_prev, int t) {
+                                                              const u8* occ_cur, u8* occ_prev, const u32* pmask,
+                                                              u32* cmask, int t) {
   if (block_stopped_before(ctrl, t)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* E = reinterpret_cast<u64*>(smem_raw);          // [7][1000] halo, then [7][640] y-pass
@@ -915,18 +917,23 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
     const int x = x0 + hx - 1, yv = y0 + hy - 1, z = z0 + hz - 1;
     if (x >= 0 && yv >= 0 && z >= 0 && x < ext0 && yv < ext1 && z < ext2) v[u] = tab.ent[x * s0 + yv * s1 + z];
   }
-  // clear the previous table in this brick (its cells are no longer read)
-  for (int q = tid; prev_occ && q < kBrick * kBrick * kBrick; q += blockDim.x) {
-    const int z = z0 + q % kBrick, yv = y0 + (q / kBrick) % kBrick, x = x0 + q / (kBrick * kBrick);
-    if (x >= ext0 || yv >= ext1 || z >= ext2) continue;
-    Entry<3>* pe = prev.ent + (x * s0 + yv * s1 + z);
-    if (pe->count) {
+  // clear the previous table in this brick (its cells are no longer read):
+  // the occupancy bitmask its own k_agg_brick3 left (pmask) names the
+  // entries, so nothing is read back
+  {
+    const u32 word = prev_occ ? pmask[(size_t)blockIdx.x * 16 + (tid >> 5)] : 0u;
+    if ((word >> (tid & 31)) & 1u) {
+      const int z = z0 + tid % kBrick, yv = y0 + (tid / kBrick) % kBrick, x = x0 + tid / (kBrick * kBrick);
+      Entry<3>* pe = prev.ent + (x * s0 + yv * s1 + z);
       pe->count = 0;
 #pragma unroll
       for (int j = 0; j < 3; ++j) { pe->hi[j] = 0; pe->lo[j] = 0; }
     }
   }
-  if (!cur_occ) return;   // no occupied cell in this brick of the table
+  if (!cur_occ) {
+    if ((tid & 31) == 0) cmask[(size_t)blockIdx.x * 16 + (tid >> 5)] = 0u;
+    return;
+  }
   int occ = 0;
 #pragma unroll
   for (int u = 0; u < HPT; ++u) {
@@ -946,6 +953,10 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
   }
   if (occ) any = 1;
   __syncthreads();
+  {
+    const unsigned bits = __ballot_sync(kFull, own[tid] != 0);   // 512 threads = the brick's cells
+    if ((tid & 31) == 0) cmask[(size_t)blockIdx.x * 16 + (tid >> 5)] = bits;
+  }
   if (!any) return;
   // z-pass: S1[hx][hy][z] = E[hx][hy][z] + E[hx][hy][z+1] + E[hx][hy][z+2]
   for (int q = tid; q < kS1; q += blockDim.x) {
