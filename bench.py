@@ -269,6 +269,13 @@ def our_arm(a):
         assert int(u[0]) == 0 and int(u[-1]) == last["k"] - 1 and u.numel() == last["k"], "bad labels"
     prof = _lib.profile(2)
     _lib.profile(0)
+    # bytes k_shift actually stored per iteration of the last run (in-place
+    # iterate, unchanged coordinate pairs are not rewritten)
+    import ctypes as _C
+    last_iters = iters_total // a.steps
+    wb = np.zeros(max(1, last_iters), dtype=np.uint64)
+    _lib.check(_lib.load().gs_fetch_shift_bytes(_lib.context(local), _lib.ptr(wb), _C.c_int32(last_iters)))
+    stored_per_launch = float(wb[:last_iters].mean()) if last_iters else 0.0
     if shard:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -281,18 +288,25 @@ def our_arm(a):
     d = 3
     # k_shift reads y and writes y' (16*d B/point); k_hist bins the input
     # once per step (later tables are derived per cell, k_derive)
-    bytes_per = {"hist": 8 * d * n_local, "shift": 16 * d * n_local}
+    # k_shift: reads y (8*d B/point) and stores the coordinate pairs that
+    # changed (at most 8*d B/point; counted on device, gs_fetch_shift_bytes)
+    bytes_per = {"hist": 8 * d * n_local, "shift": 8 * d * n_local + stored_per_launch}
     work = {"hist": a.steps, "shift": iters_total}
-    kern = max(("hist", "shift", "agg"), key=lambda k: prof[k][0])
+    # per-point kernels only: the table chain (agg, derive) runs on a side
+    # stream overlapping the shifts, so its event spans include waiting
+    kern = max(("hist", "shift"), key=lambda k: prof[k][0])
     peak, peak_src = measured_peak()
     roof = None
     if kern in bytes_per:
         alg = bytes_per[kern] * work[kern]
         achieved = alg / (prof[kern][0] / 1e3) / 1e9
-        traffic, tsrc = ncu_traffic(kern)
+        traffic, tsrc = ncu_traffic(f"k_{kern}")
         roof = {"kernel": f"k_{kern}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_launch": bytes_per[kern],
+                "bytes_note": ("k_shift: 8*d*n read + the bytes actually stored (in-place iterate; bitwise-"
+                               "unchanged coordinate pairs are not rewritten); the full rewrite would be "
+                               f"16*d*n = {16 * d * n_local} B") if kern == "shift" else None,
                 "avg_launch_ms": prof[kern][0] / work[kern], "traffic_source": tsrc}
     kernels = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
     for k in ("hist", "shift"):
@@ -306,8 +320,12 @@ def our_arm(a):
             "data": "synthetic (seeded numpy, paper_2104_00303_b200/workloads.py); fp32 input upcast "
                     "on device like PointSet (grid.py:43)",
             "config": workload_config(n, world), "iterations_per_step": per_step_iters,
-            "roofline": roof, "kernels": kernels, "gpu_launches": launches,
-            "clocks": clk.summary()}
+            "roofline": roof, "kernels": kernels,
+            "kernels_note": "CUDA-event spans per kind over the timed region; agg/derive run on a "
+                            "low-priority side stream concurrently with the shifts (their spans include "
+                            "waiting for SM slots); see profiles/launches_r01_summary.json for serialised "
+                            "per-kernel device time",
+            "gpu_launches": launches, "clocks": clk.summary()}
 
     if shard:
         line["config"]["parallelism"] = f"rows sharded over {world} GPU(s), NCCL"

@@ -127,6 +127,11 @@ GS_API int gs_fetch_modes(gs_ctx* ctx, double* modes_out, int64_t cap_rows);
  * last run (observability; pins per-iteration tables bit for bit). */
 GS_API int gs_fetch_trace(gs_ctx* ctx, int64_t* k_per_iter, uint64_t* fp_per_iter, int32_t cap);
 
+/* Bytes the shift kernel stored per iteration of the last per-point run (the
+ * iterate is updated in place and bitwise-unchanged coordinate pairs are not
+ * rewritten; reads are always 8*d bytes per point).  Roofline accounting. */
+GS_API int gs_fetch_shift_bytes(gs_ctx* ctx, uint64_t* bytes_per_iter, int32_t cap);
+
 /* Kernel accounting.  mode 1: enable per-launch CUDA-event timing (and
  * reset counters); mode 0: disable (and reset); mode 2: write the
  * accumulated device milliseconds and launch counts per kernel kind

@@ -91,7 +91,7 @@ struct gs_ctx {
   std::vector<int64_t> track_bins;
   Prof prof;
   bool collapsed = false;               // option: collapsed iterations (gs_ctx_set_option)
-  Buf runposb, runcntb, bkcnt, bktot, bocc, bmask;
+  Buf runposb, runcntb, bkcnt, bktot, bocc, bmask, wr_hist;
   bool tables_dirty = false;            // a call failed mid-run: table buffers may hold entries
   // table-chain stream (see enqueue_iteration: overlap)
   cudaStream_t side = nullptr;
@@ -376,8 +376,8 @@ template <int D, class Tab>
 void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, int64_t n, int nb_pts,
                        int nb_cells, u64* limbs = nullptr, bool with_shift = true, bool overlap = false) {
   const int cur = t & 1;
-  double* y_in = static_cast<double*>(c->y[cur].p);
-  double* y_out = static_cast<double*>(c->y[cur ^ 1].p);
+  // the iterate lives in y[0] and is shifted in place (k_shift)
+  double* y_it = static_cast<double*>(c->y[0].p);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   // overlap needs dense tables (k_shift does not read them) and 2 record buffers
   const bool ov = overlap && Tab::kDense && with_shift;
@@ -451,9 +451,10 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     GS_CUDA(cudaStreamWaitEvent(main_st, c->ev_rec[cur], 0));
   }
   if (with_shift)
-    launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_in, y_out, n, p.g, tabs[cur], rec, ctrl,
+    launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_it, y_it, n, p.g, tabs[cur], rec, ctrl,
                                                   static_cast<u64*>(c->partials.p),
-                                                  static_cast<double*>(c->mv_hist.p), t, eta, limbs); });
+                                                  static_cast<double*>(c->mv_hist.p), t, eta, limbs,
+                                                  static_cast<u64*>(c->wr_hist.p) + t); });
   if (ov) GS_CUDA(cudaEventRecord(c->ev_shift[cur], main_st));
 }
 
@@ -693,6 +694,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
   ensure<double>(c, c->mv_hist, (size_t)max_iters);
+  GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->wr_hist, (size_t)max_iters), 0, sizeof(u64) * max_iters, c->st));
   u64* fp = ensure<u64>(c, c->fp_hist, (size_t)max_iters);
   ensure<u32>(c, c->k_hist, (size_t)max_iters);
   GS_CUDA(cudaMemsetAsync(fp, 0, sizeof(u64) * max_iters, c->st));
@@ -749,7 +751,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
         enqueue_iteration<D>(c, p, tabs.hs, t, eta, n, nb_pts, nb_cells);
       if (collapsed && t == 0) {
         Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
-        const double* y1 = static_cast<const double*>(c->y[1].p);
+        const double* y1 = static_cast<const double*>(c->y[0].p);   // y_1, shifted in place
         launch(c, K_SHIFT, [&] {
           k_runs_gather<D><<<nb_cells, kThreads, 0, c->st>>>(y1, p.g.ld, sinfo.runs, &ctrl->nruns, sinfo.start,
                                                               sinfo.end, sinfo.runpos, sinfo.runcnt, sinfo.rld);
@@ -767,7 +769,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   r.iters = c->h_ctrl->iters;
   r.converged = c->h_ctrl->done != 0;
   const int e = r.iters & 1;
-  const double* yf = static_cast<const double*>(c->y[e].p);
+  const double* yf = static_cast<const double*>(c->y[0].p);   // in-place iterate
   const SortInfo* sp = (sorted && r.iters >= 1) ? &sinfo : nullptr;
   if (p.dense)
     run_extract<D>(c, p, tabs.dn, yf, n, e, labels_dev, sp, true);
@@ -809,7 +811,7 @@ void validate_run(int64_t n, int d, double h, double eta, int max_iters) {
 template <int D>
 void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_out_host, double* movement) {
   double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n) * D);
-  double* y1 = ensure<double>(c, c->y[1], (size_t)soa_ld(n) * D);
+  ensure<double>(c, c->y[1], (size_t)soa_ld(n) * D);
   ensure<Ctrl>(c, c->ctrl, 1);
   Input in{IN_F64, xdev};
   const InitStats s = run_init<D>(c, in, n, h, y0);
@@ -820,6 +822,7 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
   ensure<double>(c, c->mv_hist, 1);
+  GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->wr_hist, 1), 0, sizeof(u64), c->st));
   GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->fp_hist, 1), 0, 8, c->st));
   GS_CUDA(cudaMemsetAsync(ensure<u32>(c, c->k_hist, 1), 0, 4, c->st));
   reset_ctrl(c);
@@ -836,7 +839,7 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
     clear_table<D>(c, p, tabs.hs[1], &ctrl->k[1]);
   }
   double* aos = ensure<double>(c, c->x_stage, (size_t)n * D);
-  launch(c, K_XPOSE, [&] { k_soa_to_aos<D><<<nb_pts, kThreads, 0, c->st>>>(y1, aos, n, p.g.ld); });
+  launch(c, K_XPOSE, [&] { k_soa_to_aos<D><<<nb_pts, kThreads, 0, c->st>>>(y0, aos, n, p.g.ld); });
   check_launch();
   read_ctrl(c);
   check_flags(c->h_ctrl->error);
@@ -1005,6 +1008,7 @@ void shard_plan_d(gs_ctx* c, ShardState* sh, const InitStats& s) {
   const int nb_pts = blocks_for(c, sh->n);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
   ensure<double>(c, c->mv_hist, (size_t)sh->max_iters);
+  GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->wr_hist, (size_t)sh->max_iters), 0, 8 * sh->max_iters, c->st));
   GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->fp_hist, (size_t)sh->max_iters), 0, 8 * sh->max_iters, c->st));
   GS_CUDA(cudaMemsetAsync(ensure<u32>(c, c->k_hist, (size_t)sh->max_iters), 0, 4 * sh->max_iters, c->st));
   reset_ctrl(c);
@@ -1028,7 +1032,7 @@ void shard_components_d(gs_ctx* c, ShardState* sh, u32 offset, long long* minima
   read_ctrl(c);
   check_flags(c->h_ctrl->error);
   const int e = c->h_ctrl->iters & 1;
-  const double* yf = static_cast<const double*>(c->y[e].p);
+  const double* yf = static_cast<const double*>(c->y[0].p);   // in-place iterate
   const SortInfo* sp = (sh->sorted && c->h_ctrl->iters >= 1) ? &sh->si : nullptr;
   extract_components<D>(c, sh->p, tabs.dn, yf, sh->n, e, sp, true, offset);
   GS_CUDA(cudaMemsetAsync(minima, 0x7f, sh->p.slots * sizeof(long long), c->st));
@@ -1044,7 +1048,7 @@ template <int D>
 void shard_finish_d(gs_ctx* c, ShardState* sh, const long long* minima, int64_t* labels_dev) {
   Tabs<D> tabs = make_tabs<D>(c, sh->p);
   const int e = c->h_ctrl->iters & 1;
-  const double* yf = static_cast<const double*>(c->y[e].p);
+  const double* yf = static_cast<const double*>(c->y[0].p);   // in-place iterate
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   launch(c, K_COMP, [&] {
     k_import_minima<D, DenseTable<D>><<<blocks_for(c, (int64_t)sh->p.list_cap), kThreads, 0, c->st>>>(
@@ -1108,7 +1112,7 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
                  &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
                  &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
-                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot, &c->bocc, &c->bmask};
+                 &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot, &c->bocc, &c->bmask, &c->wr_hist};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
@@ -1252,6 +1256,16 @@ int gs_fetch_trace(gs_ctx* c, int64_t* k_per_iter, uint64_t* fp_per_iter, int32_
     for (int i = 0; i < m; ++i) {
       if (k_per_iter) k_per_iter[i] = c->iter_k[i];
       if (fp_per_iter) fp_per_iter[i] = c->iter_fp[i];
+    }
+  });
+}
+
+int gs_fetch_shift_bytes(gs_ctx* c, uint64_t* bytes_per_iter, int32_t cap) {
+  return guarded(c, [&] {
+    const int m = std::min<int>(cap, c->h_ctrl ? c->h_ctrl->iters : 0);
+    if (m > 0 && c->wr_hist.p) {
+      GS_CUDA(cudaMemcpyAsync(bytes_per_iter, c->wr_hist.p, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
     }
   });
 }
