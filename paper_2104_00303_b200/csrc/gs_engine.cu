@@ -450,7 +450,27 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     c->st = main_st;
     GS_CUDA(cudaStreamWaitEvent(main_st, c->ev_rec[cur], 0));
   }
-  if (with_shift)
+  bool tma = false;
+  if constexpr (Tab::kDense && D <= 3) {
+    // bulk-copy pipelined shift: persistent, 2 CTAs per SM
+    if (with_shift) {
+      static bool attr = false;
+      if (!attr) {
+        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)shift_tma_smem<D>()));
+        attr = true;
+      }
+      const int64_t ntiles = (n + kShiftTilePts - 1) / kShiftTilePts;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * 2));
+      launch(c, K_SHIFT, [&] {
+        k_shift_tma<D><<<grid, kThreads, shift_tma_smem<D>(), c->st>>>(
+            y_it, n, p.g, rec, ctrl, static_cast<u64*>(c->partials.p), static_cast<double*>(c->mv_hist.p), t, eta,
+            limbs, static_cast<u64*>(c->wr_hist.p) + t);
+      });
+      tma = true;
+    }
+  }
+  if (with_shift && !tma)
     launch(c, K_SHIFT, [&] { k_shift<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y_it, y_it, n, p.g, tabs[cur], rec, ctrl,
                                                   static_cast<u64*>(c->partials.p),
                                                   static_cast<double*>(c->mv_hist.p), t, eta, limbs,

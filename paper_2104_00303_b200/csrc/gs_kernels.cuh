@@ -531,72 +531,79 @@ __device__ __forceinline__ const Rec<D>& lookup_rec(const GridParams& g, const T
 // the tables in L2.  The last CTA finishes the movement reduction and
 // evaluates `movement < eta` (modeseek.py:139) on device; `wbytes` counts the
 // bytes actually stored (per-iteration trace, for the roofline accounting).
+// One quad: look up the cell records, produce y' (out), accumulate the exact
+// movement.  `in` holds points 4q..4q+3 per axis as two double2.
 template <int D, class Tab>
-__global__ void __launch_bounds__(kThreads, 3) k_shift(const double* y, double* yo, i64 n,
-                                                       GridParams g, Tab tab, const Rec<D>* __restrict__ rec,
-                                                       Ctrl* ctrl, u64* partials, double* mv_hist, int t,
-                                                       double eta, u64* limbs, u64* wbytes) {
-  if (*(volatile int*)&ctrl->done) return;
-  u64 ahi = 0, alo = 0;
-  u32 nst = 0;   // 16-byte stores issued
-  const i64 stride = (i64)gridDim.x * blockDim.x;
-  const i64 nquads = (n + 3) >> 2;
-  for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < nquads; q += stride) {
-    double2 in[D][2];
+__device__ __forceinline__ void shift_quad(const GridParams& g, const Tab& tab, const Rec<D>* __restrict__ rec,
+                                           Ctrl* ctrl, const double2 (&in)[D][2], i64 q, i64 n,
+                                           double (&out)[4][D], u64& ahi, u64& alo) {
+  bool uni = 4 * q + 3 < n;
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+    uni &= (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][0].y)) &
+           (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].x)) &
+           (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].y));
+  if (uni) {
+    double v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = in[j][0].x;
+    const Rec<D>& r = lookup_rec<D>(g, tab, rec, v, ctrl);
+    bool still = true;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld) + 2 * q;
-      in[j][0] = __ldcs(src);
-      in[j][1] = __ldcs(src + 1);
+      out[0][j] = r.t[j];
+      still &= __double_as_longlong(out[0][j]) == __double_as_longlong(v[j]);
     }
-    double out[4][D];
-    bool uni = 4 * q + 3 < n;
-#pragma unroll
-    for (int j = 0; j < D; ++j)
-      uni &= (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][0].y)) &
-             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].x)) &
-             (__double_as_longlong(in[j][0].x) == __double_as_longlong(in[j][1].y));
-    if (uni) {
-      double v[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = in[j][0].x;
-      const Rec<D>& r = lookup_rec<D>(g, tab, rec, v, ctrl);
-#pragma unroll
-      for (int j = 0; j < D; ++j) out[0][j] = r.t[j];
+    if (!still) {   // a quad at its target moves by exactly 0
       const u128 f = move_fixed<D>(g, out[0], v) << 2;
       add128(ahi, alo, (u64)(f >> 64), (u64)f);
+    }
 #pragma unroll
-      for (int j = 0; j < D; ++j) out[1][j] = out[2][j] = out[3][j] = out[0][j];
-    } else {
+    for (int j = 0; j < D; ++j) out[1][j] = out[2][j] = out[3][j] = out[0][j];
+  } else {
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        double v[D];
+    for (int m = 0; m < 4; ++m) {
+      double v[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) v[j] = (m & 1) ? in[j][m >> 1].y : in[j][m >> 1].x;
-        if (4 * q + m < n) {
-          const Rec<D>& r = lookup_rec<D>(g, tab, rec, v, ctrl);
+      for (int j = 0; j < D; ++j) v[j] = (m & 1) ? in[j][m >> 1].y : in[j][m >> 1].x;
+      if (4 * q + m < n) {
+        const Rec<D>& r = lookup_rec<D>(g, tab, rec, v, ctrl);
 #pragma unroll
-          for (int j = 0; j < D; ++j) out[m][j] = r.t[j];
-          const u128 f = move_fixed<D>(g, out[m], v);
-          add128(ahi, alo, (u64)(f >> 64), (u64)f);
-        } else {
+        for (int j = 0; j < D; ++j) out[m][j] = r.t[j];
+        const u128 f = move_fixed<D>(g, out[m], v);
+        add128(ahi, alo, (u64)(f >> 64), (u64)f);
+      } else {
 #pragma unroll
-          for (int j = 0; j < D; ++j) out[m][j] = v[j];
-        }
+        for (int j = 0; j < D; ++j) out[m][j] = v[j];
       }
     }
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      double2* dst = reinterpret_cast<double2*>(yo + (i64)j * g.ld) + 2 * q;
-      const bool same0 = (y == yo) && __double_as_longlong(out[0][j]) == __double_as_longlong(in[j][0].x) &&
-                         __double_as_longlong(out[1][j]) == __double_as_longlong(in[j][0].y);
-      const bool same1 = (y == yo) && __double_as_longlong(out[2][j]) == __double_as_longlong(in[j][1].x) &&
-                         __double_as_longlong(out[3][j]) == __double_as_longlong(in[j][1].y);
-      if (!same0) { __stcs(dst, make_double2(out[0][j], out[1][j])); ++nst; }
-      if (!same1) { __stcs(dst + 1, make_double2(out[2][j], out[3][j])); ++nst; }
-    }
   }
-  // block reduction of the 128-bit movement, last CTA finishes
+}
+
+// Store y' of a quad into yo; with an in-place iterate, 16-byte pairs whose
+// coordinates are bitwise unchanged are not rewritten.
+template <int D>
+__device__ __forceinline__ void store_quad(double* yo, i64 ld, i64 q, bool inplace, const double2 (&in)[D][2],
+                                           const double (&out)[4][D], u32& nst) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double2* dst = reinterpret_cast<double2*>(yo + (i64)j * ld) + 2 * q;
+    const bool same0 = inplace && __double_as_longlong(out[0][j]) == __double_as_longlong(in[j][0].x) &&
+                       __double_as_longlong(out[1][j]) == __double_as_longlong(in[j][0].y);
+    const bool same1 = inplace && __double_as_longlong(out[2][j]) == __double_as_longlong(in[j][1].x) &&
+                       __double_as_longlong(out[3][j]) == __double_as_longlong(in[j][1].y);
+    if (!same0) { __stcs(dst, make_double2(out[0][j], out[1][j])); ++nst; }
+    if (!same1) { __stcs(dst + 1, make_double2(out[2][j], out[3][j])); ++nst; }
+  }
+}
+
+// Block reduction of the 128-bit movement and the store count; the last CTA
+// finishes: movement < eta (modeseek.py:139) on device, or the 4 limbs of
+// this rank's exact total for a sharded run.
+template <int D>
+__device__ __forceinline__ void finish_movement(const GridParams& g, Ctrl* ctrl, u64* partials, double* mv_hist,
+                                                int t, double eta, u64* limbs, u64* wbytes, u64 ahi, u64 alo,
+                                                u32 nst) {
   const int lane = threadIdx.x & 31;
   for (int off = 16; off; off >>= 1) {
     const u64 oh = __shfl_xor_sync(kFull, ahi, off);
@@ -651,6 +658,153 @@ __global__ void __launch_bounds__(kThreads, 3) k_shift(const double* y, double* 
     ctrl->iters = t + 1;
     if (mv < eta) ctrl->done = t + 1;   // stamped: the run stopped after iteration t
   }
+}
+
+// Shift of iteration t (modeseek.py:109-110): per 4-point quad (two 16-byte
+// vector loads per SoA axis) look up the cell record, write y' = target,
+// accumulate the per-point L2 movement in 128-bit fixed point.  Quads of
+// bitwise-identical points (every cell-sorted run after iteration 0) share
+// one lookup and one norm (exact: identical inputs, movement scaled by 4 in
+// fixed point).  The iterate is updated IN PLACE (y == yo is allowed: each
+// quad is read and written by one thread only, lookups go through the cell
+// records), and a 16-byte store whose two coordinates are bitwise unchanged
+// is elided -- once clusters settle most points sit at their cell's target,
+// so converged iterations stream mostly reads.  `wbytes` counts the bytes
+// actually stored (per-iteration trace, for the roofline accounting).
+// Register-prefetched variant (any table); dense tables use k_shift_tma.
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads, 2) k_shift(const double* y, double* yo, i64 n,
+                                                       GridParams g, Tab tab, const Rec<D>* __restrict__ rec,
+                                                       Ctrl* ctrl, u64* partials, double* mv_hist, int t,
+                                                       double eta, u64* limbs, u64* wbytes) {
+  if (*(volatile int*)&ctrl->done) return;
+  u64 ahi = 0, alo = 0;
+  u32 nst = 0;   // 16-byte stores issued
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 nquads = (n + 3) >> 2;
+  // software pipelined: the next quad's loads are in flight while this one
+  // is looked up and compared
+  i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  double2 nx[D][2];
+  if (q < nquads) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld) + 2 * q;
+      nx[j][0] = __ldcs(src);
+      nx[j][1] = __ldcs(src + 1);
+    }
+  }
+  for (; q < nquads; q += stride) {
+    double2 in[D][2];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { in[j][0] = nx[j][0]; in[j][1] = nx[j][1]; }
+    if (q + stride < nquads) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld) + 2 * (q + stride);
+        nx[j][0] = __ldcs(src);
+        nx[j][1] = __ldcs(src + 1);
+      }
+    }
+    double out[4][D];
+    shift_quad<D, Tab>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
+    store_quad<D>(yo, g.ld, q, y == yo, in, out, nst);
+  }
+  finish_movement<D>(g, ctrl, partials, mv_hist, t, eta, limbs, wbytes, ahi, alo, nst);
+}
+
+// ---- TMA-pipelined shift (dense tables, in-place iterate).  A persistent
+// CTA walks tiles of 4*kThreads points; one thread keeps kShiftStages tiles
+// in flight with 1-D bulk copies (cp.async.bulk, completion on an mbarrier),
+// so the read stream needs no registers and no per-thread latency hiding.
+constexpr int kShiftTilePts = 4 * kThreads;
+constexpr int kShiftStages = 4;
+
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int D>
+constexpr size_t shift_tma_smem() {
+  return (size_t)kShiftStages * D * kShiftTilePts * sizeof(double);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) k_shift_tma(double* y, i64 n, GridParams g,
+                                                           const Rec<D>* __restrict__ rec, Ctrl* ctrl,
+                                                           u64* partials, double* mv_hist, int t, double eta,
+                                                           u64* limbs, u64* wbytes) {
+  if (*(volatile int*)&ctrl->done) return;
+  extern __shared__ __align__(128) double tiles[];   // [stage][axis][kShiftTilePts]
+  __shared__ __align__(8) u64 full[kShiftStages];
+  const DenseTable<D> tab{};
+  const i64 ntiles = (n + kShiftTilePts - 1) / kShiftTilePts;
+  const i64 G = gridDim.x;
+  const i64 mine = (ntiles > (i64)blockIdx.x) ? (ntiles - (i64)blockIdx.x + G - 1) / G : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kShiftStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](i64 k) {
+    const i64 p0 = ((i64)blockIdx.x + k * G) * kShiftTilePts;
+    const i64 cnt = min((i64)kShiftTilePts, n - p0);
+    const u32 bytes = (u32)(((cnt + 1) & ~1ll) * (i64)sizeof(double));   // 16-byte multiple (ld pads)
+    const int s = (int)(k % kShiftStages);
+    mbar_expect_tx(&full[s], bytes * D);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      bulk_g2s(tiles + ((size_t)s * D + j) * kShiftTilePts, y + (i64)j * g.ld + p0, bytes, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (i64 k = 0; k < min((i64)kShiftStages, mine); ++k) issue(k);
+  u64 ahi = 0, alo = 0;
+  u32 nst = 0;
+  for (i64 k = 0; k < mine; ++k) {
+    const int s = (int)(k % kShiftStages);
+    mbar_wait(&full[s], (u32)((k / kShiftStages) & 1));
+    const i64 q = (((i64)blockIdx.x + k * G) * kShiftTilePts >> 2) + threadIdx.x;
+    if (4 * q < n) {
+      double2 in[D][2];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double2* src = reinterpret_cast<const double2*>(tiles + ((size_t)s * D + j) * kShiftTilePts) +
+                             2 * threadIdx.x;
+        in[j][0] = src[0];
+        in[j][1] = src[1];
+      }
+      double out[4][D];
+      shift_quad<D, DenseTable<D>>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
+      store_quad<D>(y, g.ld, q, true, in, out, nst);
+    }
+    __syncthreads();   // stage s consumed: refill it
+    if (threadIdx.x == 0 && k + kShiftStages < mine) issue(k + kShiftStages);
+  }
+  finish_movement<D>(g, ctrl, partials, mv_hist, t, eta, limbs, wbytes, ahi, alo, nst);
 }
 
 // Collapsed formulation: after iteration 0 all points of a run
