@@ -187,7 +187,19 @@ def measured_peak():
 
 
 def ncu_traffic(kernel):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full summary."""
+    """Mean per-launch DRAM bytes of `kernel` over a whole engine run, from the
+    committed ncu capture profiles/<kernel>_traffic_r*.csv (all launches of
+    one run), else the --set full summary profiles/ncu_full_*.json."""
+    import csv as _csv
+
+    for f in sorted((ROOT / "profiles").glob("*_traffic_r*.csv"), reverse=True):
+        vals = {}
+        for r in _csv.reader(f.read_text().splitlines()):
+            if len(r) > 12 and kernel in r[4] and r[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r[-2], 1.0)
+                vals[r[0]] = vals.get(r[0], 0.0) + float(r[-1].replace(",", "")) * scale
+        if vals:
+            return sum(vals.values()) / len(vals), f.name
     for f in sorted((ROOT / "profiles").glob("ncu_full_*.json"), reverse=True):
         try:
             d = json.loads(f.read_text())
@@ -300,8 +312,8 @@ def our_arm(a):
     if kern in bytes_per:
         alg = bytes_per[kern] * work[kern]
         achieved = alg / (prof[kern][0] / 1e3) / 1e9
-        traffic, tsrc = ncu_traffic(f"k_{kern}")
-        roof = {"kernel": f"k_{kern}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        traffic, tsrc = ncu_traffic("k_shift_tma" if kern == "shift" else f"k_{kern}")
+        roof = {"kernel": "k_shift_tma" if kern == "shift" else f"k_{kern}", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_launch": bytes_per[kern],
                 "bytes_note": ("k_shift: 8*d*n read + the bytes actually stored (in-place iterate; bitwise-"
