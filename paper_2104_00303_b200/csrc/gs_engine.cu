@@ -398,21 +398,24 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     // (k_agg_brick3, k_derive_brick3); brick occupancy per table buffer
     const int ext0 = (int)(p.g.nkeys / p.g.stride[0]), ext1 = (int)(p.g.stride[0] / p.g.stride[1]),
               ext2 = (int)p.g.stride[1];
-    const int nbx = (ext0 + kBrick - 1) / kBrick, nby = (ext1 + kBrick - 1) / kBrick,
-              nbz = (ext2 + kBrick - 1) / kBrick;
+    const int nbx = (ext0 + kBX - 1) / kBX, nby = (ext1 + kBY - 1) / kBY, nbz = (ext2 + kBZ - 1) / kBZ;
     const int nbr = nbx * nby * nbz;
     const BrickMap bm{(u32)p.g.stride[0], (u32)p.g.stride[1], (u32)nby, (u32)nbz};
     static bool attr = false;
     if (!attr) {
       GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBrickSmem));
+      // same (maximal) shared-memory carveout as k_shift_tma, so the chain's
+      // CTAs can be co-resident with the shift's on one SM
+      GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      GS_CUDA(cudaFuncSetAttribute(k_derive_brick3, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       attr = true;
     }
     u8* occ = ensure<u8>(c, c->bocc, 2 * (size_t)nbr);
-    u32* mask = ensure<u32>(c, c->bmask, 2 * (size_t)nbr * 16);
+    u32* mask = ensure<u32>(c, c->bmask, 2 * (size_t)nbr * kMaskWords);
     if (t == 0) {
       // iteration 0 starts from a freshly built table in buffer 0
       GS_CUDA(cudaMemsetAsync(occ, 0, 2 * (size_t)nbr, c->st));
-      GS_CUDA(cudaMemsetAsync(mask, 0, 2 * (size_t)nbr * 16 * sizeof(u32), c->st));
+      GS_CUDA(cudaMemsetAsync(mask, 0, 2 * (size_t)nbr * kMaskWords * sizeof(u32), c->st));
       launch(c, K_AGG, [&] {
         k_mark_bricks<<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(
             reinterpret_cast<const Entry<3>*>(tabs[0].ent), p.slots, bm, occ);
@@ -424,7 +427,7 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
       k_agg_brick3<<<nbr, kBrickThreads, kBrickSmem, c->st>>>(
           p.g, tabs[cur], tabs[cur ^ 1], reinterpret_cast<Rec<3>*>(rec), ctrl,
           static_cast<u64*>(c->fp_hist.p) + t, static_cast<u32*>(c->k_hist.p) + t, nbx, nby, nbz, occ_cur, occ_nxt,
-          mask + (size_t)(cur ^ 1) * nbr * 16, mask + (size_t)cur * nbr * 16, t);
+          mask + (size_t)(cur ^ 1) * nbr * kMaskWords, mask + (size_t)cur * nbr * kMaskWords, t);
     });
     if (ov) GS_CUDA(cudaEventRecord(c->ev_rec[cur], c->st));
     launch(c, K_DERIVE, [&] {
@@ -456,6 +459,7 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     if (with_shift) {
       static bool attr = false;
       if (!attr) {
+        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)shift_tma_smem<D>()));
         attr = true;

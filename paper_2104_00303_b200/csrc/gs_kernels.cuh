@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_shift(const double* y, double* 
 // in flight with 1-D bulk copies (cp.async.bulk, completion on an mbarrier),
 // so the read stream needs no registers and no per-thread latency hiding.
 constexpr int kShiftTilePts = 4 * kThreads;
-constexpr int kShiftStages = 4;
+constexpr int kShiftStages = 3;
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
@@ -754,7 +754,7 @@ constexpr size_t shift_tma_smem() {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2) k_shift_tma(double* y, i64 n, GridParams g,
+__global__ void __maxnreg__(96) k_shift_tma(double* y, i64 n, GridParams g,
                                                            const Rec<D>* __restrict__ rec, Ctrl* ctrl,
                                                            u64* partials, double* mv_hist, int t, double eta,
                                                            u64* limbs, u64* wbytes) {
@@ -1023,21 +1023,27 @@ __global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Ta
 // Occupied cells then round once and divide (grid.py:230-259,
 // modeseek.py:109).  Also clears the previous table inside the brick and
 // records k and the fingerprint.
-constexpr int kBrick = 8;
-constexpr int kHalo = kBrick + 2;
-constexpr int kBrickThreads = 512;
-static_assert(kBrickThreads == kBrick * kBrick * kBrick, "one thread per brick cell (occupancy ballots)");
+// Bricks are 4 x 8 x 8 cells (x, y, z; z = the fastest key axis): 62.5 KB
+// of shared memory and 256 threads, small enough to sit on an SM next to two
+// k_shift_tma CTAs, so the side-stream table chain runs concurrently with
+// the shift instead of in its tail.
+constexpr int kBX = 4, kBY = 8, kBZ = 8;
+constexpr int kHX = kBX + 2, kHY = kBY + 2, kHZ = kBZ + 2;
+constexpr int kBrickCells = kBX * kBY * kBZ;        // 256
+constexpr int kBrickThreads = kBrickCells;
+constexpr int kMaskWords = kBrickCells / 32;        // occupancy bitmask words per brick
 constexpr int kWords3 = 7;   // count, hi[3], lo[3]
-constexpr int kH3 = kHalo * kHalo * kHalo;          // 1000: staged halo / later the y-pass
-constexpr int kS1 = kHalo * kHalo * kBrick;         // 800: z-pass
-constexpr size_t kBrickSmem = (size_t)(kH3 + kS1) * kWords3 * sizeof(u64) + kBrick * kBrick * kBrick * sizeof(u64);
+constexpr int kH3 = kHX * kHY * kHZ;                // 600: staged halo / later the y-pass
+constexpr int kS1 = kHX * kHY * kBZ;                // 480: z-pass
+constexpr int kS2 = kHX * kBY * kBZ;                // 384: y-pass
+constexpr size_t kBrickSmem = (size_t)(kH3 + kS1) * kWords3 * sizeof(u64) + kBrickCells * sizeof(u64);
 
 // Brick of a lattice slot (blockIdx order of the brick kernels).
 struct BrickMap {
   u32 s0, s1, nby, nbz;
   __device__ __forceinline__ u32 of(u32 slot) const {
     const u32 x = slot / s0, r = slot - x * s0, y = r / s1, z = r - y * s1;
-    return ((x / kBrick) * nby + y / kBrick) * nbz + z / kBrick;
+    return ((x / kBX) * nby + y / kBY) * nbz + z / kBZ;
   }
 };
 
@@ -1056,14 +1062,14 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
                                                               u32* cmask, int t) {
   if (block_stopped_before(ctrl, t)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  u64* E = reinterpret_cast<u64*>(smem_raw);          // [7][1000] halo, then [7][640] y-pass
-  u64* S1 = E + (size_t)kWords3 * kH3;                // [7][800] z-pass
-  u64* own = S1 + (size_t)kWords3 * kS1;              // [512] own counts of the brick
+  u64* E = reinterpret_cast<u64*>(smem_raw);          // [7][kH3] halo, then [7][kS2] y-pass
+  u64* S1 = E + (size_t)kWords3 * kH3;                // [7][kS1] z-pass
+  u64* own = S1 + (size_t)kWords3 * kS1;              // [kBrickCells] own counts of the brick
   __shared__ int any;
   const i64 s0 = (i64)g.stride[0], s1 = (i64)g.stride[1];
   const int ext0 = (int)((i64)g.nkeys / s0), ext1 = (int)(s0 / s1), ext2 = (int)s1;
   const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
-  const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
+  const int x0 = bx * kBX, y0 = by * kBY, z0 = bz * kBZ;
   const int tid = threadIdx.x;
   if (tid == 0) any = 0;
   const bool prev_occ = occ_prev[blockIdx.x] != 0, cur_occ = occ_cur[blockIdx.x] != 0;
@@ -1080,7 +1086,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
 #pragma unroll
     for (int j = 0; j < 3; ++j) { v[u].hi[j] = 0; v[u].lo[j] = 0; }
     if (!cur_occ || q >= kH3) continue;
-    const int hz = q % kHalo, hy = (q / kHalo) % kHalo, hx = q / (kHalo * kHalo);
+    const int hz = q % kHZ, hy = (q / kHZ) % kHY, hx = q / (kHZ * kHY);
     const int x = x0 + hx - 1, yv = y0 + hy - 1, z = z0 + hz - 1;
     if (x >= 0 && yv >= 0 && z >= 0 && x < ext0 && yv < ext1 && z < ext2) v[u] = tab.ent[x * s0 + yv * s1 + z];
   }
@@ -1088,9 +1094,9 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
   // the occupancy bitmask its own k_agg_brick3 left (pmask) names the
   // entries, so nothing is read back
   {
-    const u32 word = prev_occ ? pmask[(size_t)blockIdx.x * 16 + (tid >> 5)] : 0u;
+    const u32 word = prev_occ ? pmask[(size_t)blockIdx.x * kMaskWords + (tid >> 5)] : 0u;
     if ((word >> (tid & 31)) & 1u) {
-      const int z = z0 + tid % kBrick, yv = y0 + (tid / kBrick) % kBrick, x = x0 + tid / (kBrick * kBrick);
+      const int z = z0 + tid % kBZ, yv = y0 + (tid / kBZ) % kBY, x = x0 + tid / (kBZ * kBY);
       Entry<3>* pe = prev.ent + (x * s0 + yv * s1 + z);
       pe->count = 0;
 #pragma unroll
@@ -1098,7 +1104,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
     }
   }
   if (!cur_occ) {
-    if ((tid & 31) == 0) cmask[(size_t)blockIdx.x * 16 + (tid >> 5)] = 0u;
+    if ((tid & 31) == 0) cmask[(size_t)blockIdx.x * kMaskWords + (tid >> 5)] = 0u;
     return;
   }
   int occ = 0;
@@ -1106,56 +1112,55 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
   for (int u = 0; u < HPT; ++u) {
     const int q = tid + u * kBrickThreads;
     if (q >= kH3) continue;
-    const int hz = q % kHalo, hy = (q / kHalo) % kHalo, hx = q / (kHalo * kHalo);
+    const int hz = q % kHZ, hy = (q / kHZ) % kHY, hx = q / (kHZ * kHY);
     E[0 * kH3 + q] = v[u].count;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       E[(1 + j) * kH3 + q] = v[u].hi[j];
       E[(4 + j) * kH3 + q] = v[u].lo[j];
     }
-    if (hx >= 1 && hx <= kBrick && hy >= 1 && hy <= kBrick && hz >= 1 && hz <= kBrick) {
-      own[((hx - 1) * kBrick + (hy - 1)) * kBrick + (hz - 1)] = v[u].count;
+    if (hx >= 1 && hx <= kBX && hy >= 1 && hy <= kBY && hz >= 1 && hz <= kBZ) {
+      own[((hx - 1) * kBY + (hy - 1)) * kBZ + (hz - 1)] = v[u].count;
       occ |= v[u].count != 0;
     }
   }
   if (occ) any = 1;
   __syncthreads();
   {
-    const unsigned bits = __ballot_sync(kFull, own[tid] != 0);   // 512 threads = the brick's cells
-    if ((tid & 31) == 0) cmask[(size_t)blockIdx.x * 16 + (tid >> 5)] = bits;
+    const unsigned bits = __ballot_sync(kFull, own[tid] != 0);   // one thread per brick cell
+    if ((tid & 31) == 0) cmask[(size_t)blockIdx.x * kMaskWords + (tid >> 5)] = bits;
   }
   if (!any) return;
   // z-pass: S1[hx][hy][z] = E[hx][hy][z] + E[hx][hy][z+1] + E[hx][hy][z+2]
   for (int q = tid; q < kS1; q += blockDim.x) {
-    const int z = q % kBrick, hy = (q / kBrick) % kHalo, hx = q / (kBrick * kHalo);
-    const int b0 = (hx * kHalo + hy) * kHalo + z;
+    const int z = q % kBZ, hy = (q / kBZ) % kHY, hx = q / (kBZ * kHY);
+    const int b0 = (hx * kHY + hy) * kHZ + z;
 #pragma unroll
     for (int w = 0; w < kWords3; ++w)
       S1[w * kS1 + q] = E[w * kH3 + b0] + E[w * kH3 + b0 + 1] + E[w * kH3 + b0 + 2];
   }
   __syncthreads();
   // y-pass into E: S2[hx][y][z] = S1[hx][y][z] + S1[hx][y+1][z] + S1[hx][y+2][z]
-  constexpr int kS2 = kHalo * kBrick * kBrick;   // 640
   for (int q = tid; q < kS2; q += blockDim.x) {
-    const int z = q % kBrick, yv = (q / kBrick) % kBrick, hx = q / (kBrick * kBrick);
-    const int b0 = (hx * kHalo + yv) * kBrick + z;
+    const int z = q % kBZ, yv = (q / kBZ) % kBY, hx = q / (kBZ * kBY);
+    const int b0 = (hx * kHY + yv) * kBZ + z;
 #pragma unroll
     for (int w = 0; w < kWords3; ++w)
-      E[w * kS2 + q] = S1[w * kS1 + b0] + S1[w * kS1 + b0 + kBrick] + S1[w * kS1 + b0 + 2 * kBrick];
+      E[w * kS2 + q] = S1[w * kS1 + b0] + S1[w * kS1 + b0 + kBZ] + S1[w * kS1 + b0 + 2 * kBZ];
   }
   __syncthreads();
   // x-pass + targets for the occupied cells
   u64 fp = 0;
   u32 kc = 0;
-  for (int q = tid; q < kBrick * kBrick * kBrick; q += blockDim.x) {
+  for (int q = tid; q < kBrickCells; q += blockDim.x) {
     const u64 mine = own[q];
     if (mine == 0) continue;
-    const int lz = q % kBrick, ly = (q / kBrick) % kBrick, lx = q / (kBrick * kBrick);
-    const int b0 = (lx * kBrick + ly) * kBrick + lz;
+    const int lz = q % kBZ, ly = (q / kBZ) % kBY, lx = q / (kBZ * kBY);
+    const int b0 = (lx * kBY + ly) * kBZ + lz;
     u64 wsum[kWords3];
 #pragma unroll
     for (int w = 0; w < kWords3; ++w)
-      wsum[w] = E[w * kS2 + b0] + E[w * kS2 + b0 + kBrick * kBrick] + E[w * kS2 + b0 + 2 * kBrick * kBrick];
+      wsum[w] = E[w * kS2 + b0] + E[w * kS2 + b0 + kBY * kBZ] + E[w * kS2 + b0 + 2 * kBY * kBZ];
     const u64 slot = (u64)(x0 + lx) * s0 + (u64)(y0 + ly) * s1 + (u64)(z0 + lz);
     Rec<3> r;
     const double c = (double)wsum[0];
@@ -1225,9 +1230,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_derive_brick3(GridParams g, D
   const int ext0 = (int)((i64)g.nkeys / s0), ext1 = (int)(s0 / s1), ext2 = (int)s1;
   const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
   const int q = threadIdx.x;
-  const int z = bz * kBrick + q % kBrick, yv = by * kBrick + (q / kBrick) % kBrick,
-            x = bx * kBrick + q / (kBrick * kBrick);
-  if (x >= ext0 || yv >= ext1 || z >= ext2) return;
+  const int z = bz * kBZ + q % kBZ, yv = by * kBY + (q / kBZ) % kBY, x = bx * kBX + q / (kBZ * kBY);
   const bool inside = x < ext0 && yv < ext1 && z < ext2;
   const u32 s = inside ? (u32)(x * s0 + yv * s1 + z) : 0u;
   const u64 cnt = inside ? cur.ent[s].count : 0;
