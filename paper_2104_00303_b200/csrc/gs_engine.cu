@@ -623,8 +623,8 @@ void run_extract(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64_t 
 // holding the table of y_0 (built from shared-memory tallies) and returns
 // true.  Hash tables: per-point cursor scatter (k_scatter); table buffer 0
 // is left clean and false returned.  y[0] holds the sorted iterate after.
-template <int D, class Tab>
-bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si) {
+template <int D, class Tab, class Src>
+bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, const Src& src) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   // dense: scan every slot in key order (lexicographic cell order);
@@ -652,25 +652,27 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si) 
     const int64_t chunk = (n + nblk - 1) / nblk;
     u32* bk = ensure<u32>(c, c->bkcnt, (size_t)nblk * nb);
     u64* btot = ensure<u64>(c, c->bktot, (size_t)nb + 1);
-    double* stage = ensure<double>(c, c->stage, (size_t)n * StRec<D>::W);
-    const size_t st_smem = bk_stage_smem<D>(nb);
+    using RT = typename Src::RT;
+    constexpr int V = SRec<D, RT>::kVec;
+    uint4* stage = reinterpret_cast<uint4*>(ensure<double>(c, c->stage, (size_t)n * V * 2));
+    const size_t st_smem = bk_stage_smem<D, RT>(nb);
     static bool attr = false;
     if (!attr) {
-      GS_CUDA(cudaFuncSetAttribute(k_bk_stage<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_stage_smem<D>(2048)));
-      GS_CUDA(cudaFuncSetAttribute(k_bk_tally<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTallyWin * 4));
+      GS_CUDA(cudaFuncSetAttribute(k_bk_stage<D, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_stage_smem<D, RT>(2048)));
+      GS_CUDA(cudaFuncSetAttribute(k_bk_tally<D, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTallyWin * 4));
       attr = true;
     }
     const int nch = (int)((n + kChunkRecs - 1) / kChunkRecs);
     GS_CUDA(cudaMemsetAsync(off, 0, p.slots * sizeof(u32), c->st));
-    launch(c, K_SORT, [&] { k_bk_count<D><<<nblk, kThreads, nb * sizeof(u32), c->st>>>(y0, n, p.g, shift, nb, chunk, bk, si.cell0, ctrl); });
+    launch(c, K_SORT, [&] { k_bk_count<D, Src><<<nblk, kThreads, nb * sizeof(u32), c->st>>>(src, n, p.g, shift, nb, chunk, bk, si.cell0, ctrl); });
     launch(c, K_SORT, [&] { k_bk_cols<<<nb, 1024, 0, c->st>>>(bk, nblk, nb, btot); });
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(btot, (int)nb); });
-    launch(c, K_SORT, [&] { k_bk_stage<D><<<nblk, 512, st_smem, c->st>>>(y0, n, p.g, shift, nb, chunk, bk, btot, si.cell0, stage); });
-    launch(c, K_SORT, [&] { k_bk_tally<D><<<nch, 512, 2 * kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, off, si.minidx, ctrl); });
+    launch(c, K_SORT, [&] { k_bk_stage<D, Src><<<nblk, 512, st_smem, c->st>>>(src, n, shift, nb, chunk, bk, btot, si.cell0, stage); });
+    launch(c, K_SORT, [&] { k_bk_tally<D, RT><<<nch, 512, 2 * kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, si.minidx, ctrl); });
     launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, p.slots, off); });
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
     launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, off, p.slots, si.start, off); });
-    launch(c, K_SORT, [&] { k_bk_place<D><<<nch, 512, kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, y1); });
+    launch(c, K_SORT, [&] { k_bk_place<D, RT><<<nch, 512, kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, y1, ctrl); });
     std::swap(c->y[0], c->y[1]);
     // table 0 from the sorted iterate (runs are contiguous: cheap), then the
     // occupied-slot list of the runs
@@ -710,8 +712,13 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n) * D);
   ensure<double>(c, c->y[1], (size_t)soa_ld(n) * D);
   ensure<Ctrl>(c, c->ctrl, 1);
-  const InitStats s = run_init<D>(c, in, n, h, y0);
+  // sorted dense runs read host-layout rows straight into the sort: the
+  // statistics pass then does not materialise the fp64 iterate
+  const bool sorted = n >= kSortMinPoints;
+  const bool aos_in = in.kind == IN_F64 || in.kind == IN_F32;
+  const InitStats s = run_init<D>(c, in, n, h, (sorted && aos_in) ? nullptr : y0);
   Plan p = make_plan(n, D, h, s);
+  if (sorted && aos_in && !p.dense) run_init<D>(c, in, n, h, y0);   // hash path sorts the fp64 iterate
   Tabs<D> tabs = make_tabs<D>(c, p);
   ensure<Rec<D>>(c, c->targets, 2 * p.slots);
   const int nb_pts = blocks_for(c, n);
@@ -725,10 +732,16 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   GS_CUDA(cudaMemsetAsync(c->k_hist.p, 0, sizeof(u32) * max_iters, c->st));
   reset_ctrl(c);
   SortInfo sinfo;
-  const bool sorted = n >= kSortMinPoints;
   bool table0 = false;   // the sort already built the table of y_0
-  if (sorted)
-    table0 = p.dense ? spatial_sort<D>(c, p, tabs.dn, n, sinfo) : spatial_sort<D>(c, p, tabs.hs, n, sinfo);
+  const SrcSoA<D> soa{y0, soa_ld(n)};
+  if (sorted && !p.dense)
+    table0 = spatial_sort<D>(c, p, tabs.hs, n, sinfo, soa);
+  else if (sorted && in.kind == IN_F32)
+    table0 = spatial_sort<D>(c, p, tabs.dn, n, sinfo, SrcAoS<D, float>{static_cast<const float*>(in.dev)});
+  else if (sorted && in.kind == IN_F64)
+    table0 = spatial_sort<D>(c, p, tabs.dn, n, sinfo, SrcAoS<D, double>{static_cast<const double*>(in.dev)});
+  else if (sorted)
+    table0 = spatial_sort<D>(c, p, tabs.dn, n, sinfo, soa);
   if (sorted && !p.dense) {
     // k never grows (k_{t+1} <= k_t: y_{t+1} takes at most k_t distinct
     // values), so the loop's hash tables only need 2*k_0 slots: compact
@@ -1037,7 +1050,8 @@ void shard_plan_d(gs_ctx* c, ShardState* sh, const InitStats& s) {
   GS_CUDA(cudaMemsetAsync(ensure<u32>(c, c->k_hist, (size_t)sh->max_iters), 0, 4 * sh->max_iters, c->st));
   reset_ctrl(c);
   sh->sorted = sh->n >= kSortMinPoints;
-  const bool table0 = sh->sorted && spatial_sort<D>(c, p, tabs.dn, sh->n, sh->si);
+  const bool table0 = sh->sorted && spatial_sort<D>(c, p, tabs.dn, sh->n, sh->si,
+                                                    SrcSoA<D>{static_cast<const double*>(c->y[0].p), p.g.ld});
   if (!table0) enqueue_first_hist<D>(c, p, tabs.dn, sh->n, nb_pts);
   check_launch();
 }

@@ -149,27 +149,42 @@ struct InitStats {
   int pad;
 };
 
+// y == nullptr: statistics only (the sorted path reads x directly).  The
+// cell range is taken from the extreme coordinates: fl(v/h) and floor are
+// monotonic, so cell(min v) and cell(max v) bound every cell (grid.py:81).
 template <int D, typename T>
 __global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, double* __restrict__ y,
                                                        i64 n, i64 ld, double h, InitStats* st) {
-  i64 cmin[D], cmax[D];
-  u64 amax[D];
+  const double inv_h = 1.0 / h;
+  double vmin[D], vmax[D];
 #pragma unroll
-  for (int j = 0; j < D; ++j) { cmin[j] = LLONG_MAX; cmax[j] = LLONG_MIN; amax[j] = 0; }
+  for (int j = 0; j < D; ++j) { vmin[j] = INFINITY; vmax[j] = -INFINITY; }
   int flags = 0;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const double v = (double)x[i * D + j];
-      y[(i64)j * ld + i] = v;
+      if (y) y[(i64)j * ld + i] = v;
       if (!isfinite(v)) { flags |= kErrNonFinite; continue; }
-      const double c = cell_of(v, h);
-      if (fabs(c) >= 4611686018427387904.0) { flags |= kErrLattice; continue; }
-      const i64 ci = (i64)c;
-      cmin[j] = min(cmin[j], ci);
-      cmax[j] = max(cmax[j], ci);
-      amax[j] = max(amax[j], (u64)__double_as_longlong(fabs(v)));
+      vmin[j] = fmin(vmin[j], v);
+      vmax[j] = fmax(vmax[j], v);
+    }
+  }
+  i64 cmin[D], cmax[D];
+  u64 amax[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    cmin[j] = LLONG_MAX; cmax[j] = LLONG_MIN; amax[j] = 0;
+    if (vmin[j] <= vmax[j]) {
+      const double c0 = cell_of_fast(vmin[j], h, inv_h), c1 = cell_of_fast(vmax[j], h, inv_h);
+      if (fabs(c0) >= 4611686018427387904.0 || fabs(c1) >= 4611686018427387904.0) {
+        flags |= kErrLattice;
+      } else {
+        cmin[j] = (i64)c0;
+        cmax[j] = (i64)c1;
+      }
+      amax[j] = (u64)__double_as_longlong(fmax(fabs(vmin[j]), fabs(vmax[j])));
     }
   }
 #pragma unroll
@@ -1661,13 +1676,85 @@ __global__ void __launch_bounds__(kThreads) k_labels_runs(const u32* __restrict_
 //                one global atomic pair per (chunk, slot) -> run sizes + minima
 //   (scan of the run sizes over slots -> run starts / cursors)
 //   k_bk_place   per chunk again: per-slot cursor bump once per (chunk, slot),
-//                warp-aggregated local ranks, SoA writes of the sorted iterate
+//                shared-memory local ranks, SoA fp64 writes of the sorted iterate
+// The passes read the INPUT rows directly (SrcAoS: fp32/fp64 (n, d) as the
+// caller passed them, upcast exactly like PointSet, grid.py:43) or the fp64
+// iterate (SrcSoA, image features).  Staging records carry the source-type
+// coordinates and the original index only (16 B for fp32 d=3); the slot is
+// recomputed from the coordinates where needed (bitwise the same key).
 // Chunks whose slots span more than the shared-memory window fall back to
 // per-record global atomics (correct, just slower; never seen on the configs).
-template <int D>
-struct StRec {
-  static constexpr int W = ((D + 1) + 1) & ~1;   // D coords + (slot<<32 | index) + pad
+template <int D, typename T>
+struct SrcAoS {
+  using RT = T;
+  const T* x;
+  __device__ __forceinline__ void raw(i64 i, RT (&r)[D]) const {
+#pragma unroll
+    for (int j = 0; j < D; ++j) r[j] = __ldcs(x + i * D + j);
+  }
 };
+
+template <int D>
+struct SrcSoA {
+  using RT = double;
+  const double* y;
+  i64 ld;
+  __device__ __forceinline__ void raw(i64 i, RT (&r)[D]) const {
+#pragma unroll
+    for (int j = 0; j < D; ++j) r[j] = __ldcs(y + (i64)j * ld + i);
+  }
+};
+
+// Staging record: D coordinates of type RT, then the original index; padded
+// to whole 16-byte vectors.
+template <int D, typename RT>
+struct SRec {
+  static constexpr int kBytes = ((int)(D * sizeof(RT)) + 4 + 15) & ~15;
+  static constexpr int kVec = kBytes / 16;    // uint4 per record
+  static constexpr int kIdxWord = (int)(D * sizeof(RT)) / 4;
+};
+
+template <int D, typename RT>
+__device__ __forceinline__ void srec_put(u32* w, const RT (&r)[D], u32 idx) {
+  RT* c = reinterpret_cast<RT*>(w);
+#pragma unroll
+  for (int j = 0; j < D; ++j) c[j] = r[j];
+  w[SRec<D, RT>::kIdxWord] = idx;
+#pragma unroll
+  for (int k = SRec<D, RT>::kIdxWord + 1; k < SRec<D, RT>::kBytes / 4; ++k) w[k] = 0u;
+}
+
+// slot of a staged record (the upcast is exact, so this is the key k_bk_count saw)
+template <int D, typename RT>
+__device__ __forceinline__ u32 srec_slot(const GridParams& g, const uint4* rec, double (&v)[D], u32& idx,
+                                         bool& inside) {
+  u32 w[SRec<D, RT>::kBytes / 4];
+#pragma unroll
+  for (int k = 0; k < SRec<D, RT>::kVec; ++k) {
+    const uint4 q = rec[k];
+    w[4 * k] = q.x; w[4 * k + 1] = q.y; w[4 * k + 2] = q.z; w[4 * k + 3] = q.w;
+  }
+  const RT* c = reinterpret_cast<const RT*>(w);
+#pragma unroll
+  for (int j = 0; j < D; ++j) v[j] = (double)c[j];
+  idx = w[SRec<D, RT>::kIdxWord];
+  return (u32)pack_key<D>(g, v, inside);
+}
+
+// coordinates of a staged record, upcast
+template <int D, typename RT>
+__device__ __forceinline__ void srec_coords(const uint4* rec, double (&v)[D]) {
+  u32 w[SRec<D, RT>::kBytes / 4];
+#pragma unroll
+  for (int k = 0; k < SRec<D, RT>::kVec; ++k) {
+    const uint4 q = rec[k];
+    w[4 * k] = q.x; w[4 * k + 1] = q.y; w[4 * k + 2] = q.z; w[4 * k + 3] = q.w;
+  }
+  const RT* c = reinterpret_cast<const RT*>(w);
+#pragma unroll
+  for (int j = 0; j < D; ++j) v[j] = (double)c[j];
+}
+
 constexpr int kChunkRecs = 4096;
 constexpr int kBucketShiftMin = 12;        // >= 4096 slots per coarse bucket
 constexpr int kTallyWin = 2 << kBucketShiftMin;   // a chunk spans <= 2 buckets when they are full
@@ -1687,10 +1774,10 @@ __device__ __forceinline__ u32 smem_bump(u32* ctr, u32 key, bool valid) {
   return valid ? atomicAdd(ctr + key, 1u) : 0u;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads) k_bk_count(const double* __restrict__ y, i64 n, GridParams g,
-                                                       int shift, u32 nb, i64 chunk, u32* blk_counts,
-                                                       u32* cell0, Ctrl* ctrl) {
+template <int D, class Src>
+__global__ void __launch_bounds__(kThreads) k_bk_count(Src src, i64 n, GridParams g, int shift, u32 nb, i64 chunk,
+                                                       u32* blk_counts, u32* cell0, Ctrl* ctrl) {
+  using RT = typename Src::RT;
   extern __shared__ u32 hist[];
   for (u32 b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
   __syncthreads();
@@ -1699,9 +1786,11 @@ __global__ void __launch_bounds__(kThreads) k_bk_count(const double* __restrict_
     const i64 i = base + threadIdx.x;
     u32 bk = 0xffffffffu;
     if (i < a1) {
+      RT r[D];
+      src.raw(i, r);
       double v[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = __ldcs(y + (i64)j * g.ld + i);
+      for (int j = 0; j < D; ++j) v[j] = (double)r[j];
       bool inside;
       const u64 key = pack_key<D>(g, v, inside);
       if (!inside) {
@@ -1753,7 +1842,7 @@ __global__ void __launch_bounds__(1024) k_bk_cols(u32* blk_counts, u32 nblk, u32
   if (threadIdx.x == 0) bucket_tot[b] = carry;
 }
 
-// block-wide exclusive scan of n32 counters in shared memory (in place into out)
+// block-wide exclusive scan of nitems counters in shared memory
 __device__ __forceinline__ void block_exclusive_scan(const u32* in, u32* out, u32 nitems, u32* warpsum) {
   const u32 per = (nitems + blockDim.x - 1) / blockDim.x;
   const u32 q0 = threadIdx.x * per;
@@ -1777,27 +1866,28 @@ __device__ __forceinline__ void block_exclusive_scan(const u32* in, u32* out, u3
   __syncthreads();
 }
 
-template <int D>
-constexpr int kStageRound = (D <= 4) ? 2048 : 1024;
+template <int D, typename RT>
+constexpr int kStageRound = (SRec<D, RT>::kBytes <= 32) ? 2048 : 1024;
 
-template <int D>
+template <int D, typename RT>
 __host__ __device__ constexpr size_t bk_stage_smem(u32 nb) {
-  return (size_t)kStageRound<D> * (StRec<D>::W * 8 + 4) + (size_t)3 * nb * 4;
+  return (size_t)kStageRound<D, RT> * (SRec<D, RT>::kBytes + 4) + (size_t)3 * nb * 4;
 }
 
-template <int D>
-__global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, i64 n, GridParams g, int shift,
-                                                  u32 nb, i64 chunk, const u32* blk_off, const u64* bucket_base,
-                                                  const u32* __restrict__ cell0, double* __restrict__ stage) {
-  constexpr int W = StRec<D>::W;
-  constexpr int R = kStageRound<D>;
+template <int D, class Src>
+__global__ void __launch_bounds__(512) k_bk_stage(Src src, i64 n, int shift, u32 nb, i64 chunk, const u32* blk_off,
+                                                  const u64* bucket_base, const u32* __restrict__ cell0,
+                                                  uint4* __restrict__ stage) {
+  using RT = typename Src::RT;
+  constexpr int R = kStageRound<D, RT>;
   constexpr int PER = R / 512;
+  constexpr int V = SRec<D, RT>::kVec;
   extern __shared__ __align__(16) unsigned char raw[];
-  double* recs = reinterpret_cast<double*>(raw);                   // [R][W]
-  u32* rbk = reinterpret_cast<u32*>(recs + (size_t)R * W);         // [R] bucket of local record
-  u32* gcur = rbk + R;                                             // [nb] global cursor
-  u32* lcnt = gcur + nb;                                           // [nb] round counts
-  u32* lst = lcnt + nb;                                            // [nb] round starts
+  uint4* recs = reinterpret_cast<uint4*>(raw);                    // [R][V]
+  u32* rbk = reinterpret_cast<u32*>(recs + (size_t)R * V);        // [R] bucket of local record
+  u32* gcur = rbk + R;                                            // [nb] global cursor
+  u32* lcnt = gcur + nb;                                          // [nb] round counts
+  u32* lst = lcnt + nb;                                           // [nb] round starts
   __shared__ u32 warpsum[32];
   for (u32 b = threadIdx.x; b < nb; b += blockDim.x)
     gcur[b] = (u32)bucket_base[b] + blk_off[(i64)blockIdx.x * nb + b];
@@ -1810,13 +1900,12 @@ __global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, 
     // all global loads of the round first (memory-level parallelism), then
     // local ranks per bucket
     u32 mykey[PER], mybk[PER], myrk[PER];
-    double myv[PER][D];
+    RT myv[PER][D];
 #pragma unroll
     for (int t = 0; t < PER; ++t) {
       const int q = t * 512 + threadIdx.x;
       mykey[t] = q < m ? __ldcs(cell0 + r0 + q) : 0xffffffffu;
-#pragma unroll
-      for (int j = 0; j < D; ++j) myv[t][j] = q < m ? __ldcs(y + (i64)j * g.ld + r0 + q) : 0.0;
+      if (q < m) src.raw(r0 + q, myv[t]);
     }
 #pragma unroll
     for (int t = 0; t < PER; ++t) {
@@ -1832,12 +1921,7 @@ __global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, 
       const int q = t * 512 + threadIdx.x;
       if (mybk[t] == 0xffffffffu) continue;
       const u32 lpos = lst[mybk[t]] + myrk[t];
-      double* rec = recs + (size_t)lpos * W;
-#pragma unroll
-      for (int j = 0; j < D; ++j) rec[j] = myv[t][j];
-      rec[D] = __longlong_as_double((long long)(((u64)mykey[t] << 32) | (u64)(u32)(r0 + q)));
-#pragma unroll
-      for (int j = D + 1; j < W; ++j) rec[j] = 0.0;
+      srec_put<D, RT>(reinterpret_cast<u32*>(recs + (size_t)lpos * V), myv[t], (u32)(r0 + q));
       rbk[lpos] = mybk[t];
     }
     __syncthreads();
@@ -1847,10 +1931,8 @@ __global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, 
       const u32 bk = rbk[q];
       if (bk == 0xffffffffu) continue;
       const u32 pos = gcur[bk] + (q - lst[bk]);
-      const double2* src = reinterpret_cast<const double2*>(recs + (size_t)q * W);
-      double2* dst = reinterpret_cast<double2*>(stage + (i64)pos * W);
 #pragma unroll
-      for (int w = 0; w < W / 2; ++w) dst[w] = src[w];
+      for (int w = 0; w < V; ++w) stage[(i64)pos * V + w] = recs[(size_t)q * V + w];
       rbk[q] = 0xffffffffu;
     }
     __syncthreads();
@@ -1860,31 +1942,38 @@ __global__ void __launch_bounds__(512) k_bk_stage(const double* __restrict__ y, 
 }
 
 // A chunk = kChunkRecs staging records, kRpt per thread of a 512-thread
-// block (record r0 + t*512 + tid); each thread keeps its records' tags
-// (slot << 32 | original index) in registers across the passes.
+// block (record r0 + t*512 + tid); each thread keeps its records' slots and
+// indices in registers across the passes.
 constexpr int kRpt = kChunkRecs / 512;
 
-template <int D>
-__device__ __forceinline__ void load_tags(const double* __restrict__ stage, i64 r0, i64 r1, u64 (&tag)[kRpt]) {
-  constexpr int W = StRec<D>::W;
+template <int D, typename RT>
+__device__ __forceinline__ void load_slots(const uint4* __restrict__ stage, const GridParams& g, i64 r0, i64 r1,
+                                           u32 (&key)[kRpt], u32 (&idx)[kRpt], Ctrl* ctrl) {
+  constexpr int V = SRec<D, RT>::kVec;
 #pragma unroll
   for (int t = 0; t < kRpt; ++t) {
     const i64 r = r0 + t * 512 + threadIdx.x;
-    tag[t] = r < r1 ? (u64)__double_as_longlong(stage[r * W + D]) : ~0ull;
+    key[t] = 0xffffffffu;
+    idx[t] = 0xffffffffu;
+    if (r < r1) {
+      double v[D];
+      bool inside;
+      const u32 k = srec_slot<D, RT>(g, stage + r * V, v, idx[t], inside);
+      if (inside) key[t] = k; else atomicOr(&ctrl->error, kErrMissing);
+    }
   }
 }
 
 // slot range [kmin, kmax] of the chunk (block-wide)
-__device__ __forceinline__ void tags_range(const u64 (&tag)[kRpt], u32* kmin_s, u32* kmax_s) {
+__device__ __forceinline__ void slots_range(const u32 (&key)[kRpt], u32* kmin_s, u32* kmax_s) {
   if (threadIdx.x == 0) { *kmin_s = 0xffffffffu; *kmax_s = 0; }
   __syncthreads();
   u32 lmin = 0xffffffffu, lmax = 0;
 #pragma unroll
   for (int t = 0; t < kRpt; ++t) {
-    if (tag[t] == ~0ull) continue;
-    const u32 key = (u32)(tag[t] >> 32);
-    lmin = min(lmin, key);
-    lmax = max(lmax, key);
+    if (key[t] == 0xffffffffu) continue;
+    lmin = min(lmin, key[t]);
+    lmax = max(lmax, key[t]);
   }
   lmin = __reduce_min_sync(kFull, lmin);
   lmax = __reduce_max_sync(kFull, lmax);
@@ -1898,18 +1987,18 @@ __device__ __forceinline__ void tags_range(const u64 (&tag)[kRpt], u32* kmin_s, 
 // per chunk of staging: per-slot counts and minimum original index through
 // shared-memory tallies over the chunk's slot window, then one global atomic
 // pair per (chunk, slot).  cnt must be zero on entry.
-template <int D>
-__global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ stage, i64 n, u64 nslots, u32* cnt,
-                                                  u32* minidx, Ctrl* ctrl) {
+template <int D, typename RT>
+__global__ void __launch_bounds__(512) k_bk_tally(const uint4* __restrict__ stage, i64 n, u64 nslots, GridParams g,
+                                                  u32* cnt, u32* minidx, Ctrl* ctrl) {
   constexpr int WIN = kTallyWin;
   extern __shared__ u32 tsm[];
   u32* lc = tsm;
   u32* mn = tsm + WIN;
   __shared__ u32 kmin_s, kmax_s;
   const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
-  u64 tag[kRpt];
-  load_tags<D>(stage, r0, r1, tag);
-  tags_range(tag, &kmin_s, &kmax_s);
+  u32 key[kRpt], idx[kRpt];
+  load_slots<D, RT>(stage, g, r0, r1, key, idx, ctrl);
+  slots_range(key, &kmin_s, &kmax_s);
   const u32 kmin = kmin_s;
   const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
   const u32 span = wide ? 0 : kmax_s - kmin + 1;
@@ -1920,30 +2009,25 @@ __global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ sta
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < kRpt; ++t) {
-    const bool valid = tag[t] != ~0ull;
-    const u32 key = (u32)(tag[t] >> 32), idx = (u32)tag[t];
+    const bool valid = key[t] != 0xffffffffu;
     if (wide) {
-      if (valid) {
-        if (key >= nslots) {
-          atomicOr(&ctrl->error, kErrMissing);
-        } else {
-          atomicAdd(cnt + key, 1u);
-          atomicMin(minidx + key, idx);
-        }
+      if (valid && key[t] < nslots) {
+        atomicAdd(cnt + key[t], 1u);
+        atomicMin(minidx + key[t], idx[t]);
       }
       continue;
     }
     // one atomic pair for a warp on a single slot (hot cells), else per lane
-    const u32 k0 = __shfl_sync(kFull, key, 0);
-    if (__all_sync(kFull, valid && key == k0)) {
-      const u32 mnv = __reduce_min_sync(kFull, idx);
+    const u32 k0 = __shfl_sync(kFull, key[t], 0);
+    if (__all_sync(kFull, valid && key[t] == k0)) {
+      const u32 mnv = __reduce_min_sync(kFull, idx[t]);
       if ((threadIdx.x & 31) == 0) {
         atomicAdd(lc + (k0 - kmin), 32u);
         atomicMin(mn + (k0 - kmin), mnv);
       }
     } else if (valid) {
-      atomicAdd(lc + (key - kmin), 1u);
-      atomicMin(mn + (key - kmin), idx);
+      atomicAdd(lc + (key[t] - kmin), 1u);
+      atomicMin(mn + (key[t] - kmin), idx[t]);
     }
   }
   __syncthreads();
@@ -1955,18 +2039,18 @@ __global__ void __launch_bounds__(512) k_bk_tally(const double* __restrict__ sta
 }
 
 // per chunk again: one global cursor bump per (chunk, slot), shared-memory
-// local ranks, SoA writes of the sorted iterate (off ends as run ends)
-template <int D>
-__global__ void __launch_bounds__(512) k_bk_place(const double* __restrict__ stage, i64 n, u64 nslots, GridParams g,
-                                                  u32* off, double* __restrict__ ys) {
-  constexpr int W = StRec<D>::W;
+// local ranks, SoA fp64 writes of the sorted iterate (off ends as run ends)
+template <int D, typename RT>
+__global__ void __launch_bounds__(512) k_bk_place(const uint4* __restrict__ stage, i64 n, u64 nslots, GridParams g,
+                                                  u32* off, double* __restrict__ ys, Ctrl* ctrl) {
   constexpr int WIN = kTallyWin;
+  constexpr int V = SRec<D, RT>::kVec;
   extern __shared__ u32 cnt[];
   __shared__ u32 kmin_s, kmax_s;
   const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
-  u64 tag[kRpt];
-  load_tags<D>(stage, r0, r1, tag);
-  tags_range(tag, &kmin_s, &kmax_s);
+  u32 key[kRpt], idx[kRpt];
+  load_slots<D, RT>(stage, g, r0, r1, key, idx, ctrl);
+  slots_range(key, &kmin_s, &kmax_s);
   const u32 kmin = kmin_s;
   const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
   u32 pos[kRpt];
@@ -1975,28 +2059,28 @@ __global__ void __launch_bounds__(512) k_bk_place(const double* __restrict__ sta
     for (u32 q = threadIdx.x; q < span; q += blockDim.x) cnt[q] = 0;
     __syncthreads();
 #pragma unroll
-    for (int t = 0; t < kRpt; ++t) pos[t] = smem_bump(cnt, (u32)(tag[t] >> 32) - kmin, tag[t] != ~0ull);
+    for (int t = 0; t < kRpt; ++t) pos[t] = smem_bump(cnt, key[t] - kmin, key[t] != 0xffffffffu);
     __syncthreads();
     for (u32 q = threadIdx.x; q < span; q += blockDim.x)
       if (cnt[q]) cnt[q] = atomicAdd(off + kmin + q, cnt[q]);   // now the chunk's base
     __syncthreads();
 #pragma unroll
     for (int t = 0; t < kRpt; ++t)
-      if (tag[t] != ~0ull) pos[t] += cnt[(u32)(tag[t] >> 32) - kmin];
+      if (key[t] != 0xffffffffu) pos[t] += cnt[key[t] - kmin];
   } else {
 #pragma unroll
     for (int t = 0; t < kRpt; ++t) {
-      const u32 key = (u32)(tag[t] >> 32);
-      if (tag[t] != ~0ull && key >= nslots) tag[t] = ~0ull;
-      pos[t] = tag[t] != ~0ull ? atomicAdd(off + key, 1u) : 0u;
+      if (key[t] >= nslots) key[t] = 0xffffffffu;
+      pos[t] = key[t] != 0xffffffffu ? atomicAdd(off + key[t], 1u) : 0u;
     }
   }
 #pragma unroll
   for (int t = 0; t < kRpt; ++t) {
-    if (tag[t] == ~0ull || pos[t] >= (u32)n) continue;
-    const double* rec = stage + (r0 + t * 512 + threadIdx.x) * W;
+    if (key[t] == 0xffffffffu || pos[t] >= (u32)n) continue;
+    double v[D];
+    srec_coords<D, RT>(stage + (r0 + t * 512 + threadIdx.x) * V, v);
 #pragma unroll
-    for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * g.ld + pos[t], rec[j]);
+    for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * g.ld + pos[t], v[j]);
   }
 }
 
