@@ -1041,7 +1041,7 @@ void shard_plan_d(gs_ctx* c, ShardState* sh, const InitStats& s) {
   p.g.ld = soa_ld(sh->n);
   sh->p = p;
   Tabs<D> tabs = make_tabs<D>(c, p);
-  ensure<Rec<D>>(c, c->targets, p.slots);
+  ensure<Rec<D>>(c, c->targets, 2 * p.slots);
   const int nb_pts = blocks_for(c, sh->n);
   ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
   ensure<double>(c, c->mv_hist, (size_t)sh->max_iters);
@@ -1060,13 +1060,14 @@ template <int D>
 void shard_iterate_d(gs_ctx* c, ShardState* sh, int t, u64* limbs) {
   Tabs<D> tabs = make_tabs<D>(c, sh->p);
   enqueue_iteration<D>(c, sh->p, tabs.dn, t, 0.0, sh->n, blocks_for(c, sh->n),
-                       blocks_for(c, (int64_t)sh->p.list_cap), limbs);
+                       blocks_for(c, (int64_t)sh->p.list_cap), limbs, true, true);
   check_launch();
 }
 
 template <int D>
 void shard_components_d(gs_ctx* c, ShardState* sh, u32 offset, long long* minima) {
   Tabs<D> tabs = make_tabs<D>(c, sh->p);
+  side_join(c);
   read_ctrl(c);
   check_flags(c->h_ctrl->error);
   const int e = c->h_ctrl->iters & 1;
@@ -1545,6 +1546,7 @@ int gs_shard_status(gs_ctx* c, int32_t* done_out, int32_t* iters_out, void* stre
   return guarded(c, [&] {
     c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
     shard_of(c, false);
+    side_join(c);   // the table chain may run ahead on the side stream
     read_ctrl(c);
     check_flags(c->h_ctrl->error);
     *done_out = c->h_ctrl->done != 0;
