@@ -479,7 +479,10 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
                                                   static_cast<u64*>(c->partials.p),
                                                   static_cast<double*>(c->mv_hist.p), t, eta, limbs,
                                                   static_cast<u64*>(c->wr_hist.p) + t); });
-  if (ov) GS_CUDA(cudaEventRecord(c->ev_shift[cur], main_st));
+  // ev_shift[cur] releases the chain two iterations ahead; it must follow
+  // the stop decision of iteration t (in the shift itself, or k_converge for
+  // a sharded run -- gs_shard_converge records it there)
+  if (ov && !limbs) GS_CUDA(cudaEventRecord(c->ev_shift[cur], main_st));
 }
 
 // Collapsed iteration t >= 1: targets + derived table as usual, then one
@@ -1538,6 +1541,7 @@ int gs_shard_converge(gs_ctx* c, int32_t t, const void* limbs_dev, double eta, v
       k_converge<<<1, 1, 0, c->st>>>(static_cast<const u64*>(limbs_dev), sh->p.g, static_cast<Ctrl*>(c->ctrl.p),
                                      static_cast<double*>(c->mv_hist.p), t, eta);
     });
+    if (c->side) GS_CUDA(cudaEventRecord(c->ev_shift[t & 1], c->st));   // see enqueue_iteration
     check_launch();
   });
 }
