@@ -1052,6 +1052,7 @@ constexpr int kH3 = kHX * kHY * kHZ;                // 600: staged halo / later 
 constexpr int kS1 = kHX * kHY * kBZ;                // 480: z-pass
 constexpr int kS2 = kHX * kBY * kBZ;                // 384: y-pass
 constexpr size_t kBrickSmem = (size_t)(kH3 + kS1) * kWords3 * sizeof(u64) + kBrickCells * sizeof(u64);
+constexpr int kSparseCells = 48;   // at most this many occupied cells: direct 27-point gathers
 
 // Brick of a lattice slot (blockIdx order of the brick kernels).
 struct BrickMap {
@@ -1140,42 +1141,66 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
     }
   }
   if (occ) any = 1;
+  __shared__ int nocc;
+  if (tid == 0) nocc = 0;
   __syncthreads();
   {
     const unsigned bits = __ballot_sync(kFull, own[tid] != 0);   // one thread per brick cell
-    if ((tid & 31) == 0) cmask[(size_t)blockIdx.x * kMaskWords + (tid >> 5)] = bits;
+    if ((tid & 31) == 0) {
+      cmask[(size_t)blockIdx.x * kMaskWords + (tid >> 5)] = bits;
+      if (bits) atomicAdd(&nocc, __popc(bits));
+    }
   }
   if (!any) return;
-  // z-pass: S1[hx][hy][z] = E[hx][hy][z] + E[hx][hy][z+1] + E[hx][hy][z+2]
-  for (int q = tid; q < kS1; q += blockDim.x) {
-    const int z = q % kBZ, hy = (q / kBZ) % kHY, hx = q / (kBZ * kHY);
-    const int b0 = (hx * kHY + hy) * kHZ + z;
-#pragma unroll
-    for (int w = 0; w < kWords3; ++w)
-      S1[w * kS1 + q] = E[w * kH3 + b0] + E[w * kH3 + b0 + 1] + E[w * kH3 + b0 + 2];
-  }
   __syncthreads();
-  // y-pass into E: S2[hx][y][z] = S1[hx][y][z] + S1[hx][y+1][z] + S1[hx][y+2][z]
-  for (int q = tid; q < kS2; q += blockDim.x) {
-    const int z = q % kBZ, yv = (q / kBZ) % kBY, hx = q / (kBZ * kBY);
-    const int b0 = (hx * kHY + yv) * kBZ + z;
+  // sparse brick (few occupied cells, typical once clusters contract): each
+  // occupied cell gathers its 27 neighbours from the staged halo directly;
+  // dense brick: separable z, y, x passes over the whole brick
+  const bool sparse = nocc <= kSparseCells;
+  if (!sparse) {
+    // z-pass: S1[hx][hy][z] = E[hx][hy][z] + E[hx][hy][z+1] + E[hx][hy][z+2]
+    for (int q = tid; q < kS1; q += blockDim.x) {
+      const int z = q % kBZ, hy = (q / kBZ) % kHY, hx = q / (kBZ * kHY);
+      const int b0 = (hx * kHY + hy) * kHZ + z;
 #pragma unroll
-    for (int w = 0; w < kWords3; ++w)
-      E[w * kS2 + q] = S1[w * kS1 + b0] + S1[w * kS1 + b0 + kBZ] + S1[w * kS1 + b0 + 2 * kBZ];
+      for (int w = 0; w < kWords3; ++w)
+        S1[w * kS1 + q] = E[w * kH3 + b0] + E[w * kH3 + b0 + 1] + E[w * kH3 + b0 + 2];
+    }
+    __syncthreads();
+    // y-pass into E: S2[hx][y][z] = S1[hx][y][z] + S1[hx][y+1][z] + S1[hx][y+2][z]
+    for (int q = tid; q < kS2; q += blockDim.x) {
+      const int z = q % kBZ, yv = (q / kBZ) % kBY, hx = q / (kBZ * kBY);
+      const int b0 = (hx * kHY + yv) * kBZ + z;
+#pragma unroll
+      for (int w = 0; w < kWords3; ++w)
+        E[w * kS2 + q] = S1[w * kS1 + b0] + S1[w * kS1 + b0 + kBZ] + S1[w * kS1 + b0 + 2 * kBZ];
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // x-pass + targets for the occupied cells
+  // x-pass (or direct gather) + targets for the occupied cells
   u64 fp = 0;
   u32 kc = 0;
   for (int q = tid; q < kBrickCells; q += blockDim.x) {
     const u64 mine = own[q];
     if (mine == 0) continue;
     const int lz = q % kBZ, ly = (q / kBZ) % kBY, lx = q / (kBZ * kBY);
-    const int b0 = (lx * kBY + ly) * kBZ + lz;
     u64 wsum[kWords3];
+    if (sparse) {
 #pragma unroll
-    for (int w = 0; w < kWords3; ++w)
-      wsum[w] = E[w * kS2 + b0] + E[w * kS2 + b0 + kBY * kBZ] + E[w * kS2 + b0 + 2 * kBY * kBZ];
+      for (int w = 0; w < kWords3; ++w) wsum[w] = 0;
+      for (int dx = 0; dx < 3; ++dx)
+        for (int dy = 0; dy < 3; ++dy) {
+          const int h0 = ((lx + dx) * kHY + (ly + dy)) * kHZ + lz;
+#pragma unroll
+          for (int w = 0; w < kWords3; ++w)
+            wsum[w] += E[w * kH3 + h0] + E[w * kH3 + h0 + 1] + E[w * kH3 + h0 + 2];
+        }
+    } else {
+      const int b0 = (lx * kBY + ly) * kBZ + lz;
+#pragma unroll
+      for (int w = 0; w < kWords3; ++w)
+        wsum[w] = E[w * kS2 + b0] + E[w * kS2 + b0 + kBY * kBZ] + E[w * kS2 + b0 + 2 * kBY * kBZ];
+    }
     const u64 slot = (u64)(x0 + lx) * s0 + (u64)(y0 + ly) * s1 + (u64)(z0 + lz);
     Rec<3> r;
     const double c = (double)wsum[0];
