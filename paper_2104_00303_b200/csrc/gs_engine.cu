@@ -544,7 +544,7 @@ void extract_components(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, i
   }
   u32* par = ensure<u32>(c, c->par, p.slots);
   u32* first = ensure<u32>(c, c->first, p.slots);
-  launch(c, K_COMP, [&] { k_uf_init<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, first); });
+  launch(c, K_COMP, [&] { k_uf_init<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[e], &ctrl->k[e], par, first); });
   launch(c, K_COMP, [&] { k_uf_link<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[e], &ctrl->k[e], par); });
   launch(c, K_COMP, [&] { k_uf_flatten<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(tabs[e], &ctrl->k[e], par, tabs[e ^ 1].ent); });
   if (si)

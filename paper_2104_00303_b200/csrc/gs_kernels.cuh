@@ -2147,13 +2147,31 @@ __device__ __forceinline__ void uf_unite(u32* par, u32 a, u32 b) {
   }
 }
 
+// par[s] = the first occupied lexicographically earlier neighbour with a
+// smaller slot (ECL-CC style initial hooking: most unions of k_uf_link then
+// find their roots already equal), else s.
 template <int D, class Tab>
-__global__ void k_uf_init(Tab tab, const u32* kp, u32* par, u32* first) {
+__global__ void k_uf_init(GridParams g, Tab tab, const u32* kp, u32* par, u32* first) {
+  constexpr int M = (D == 1) ? 3 : (D == 2) ? 9 : (D == 3) ? 27 : (D == 4) ? 81 :
+                    (D == 5) ? 243 : (D == 6) ? 729 : (D == 7) ? 2187 : 6561;
   const u32 k = *kp;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
     const u32 s = tab.list[a];
-    par[s] = s;
+    const u64 key = tab.key_of(s);
+    u32 p = s;
+    for (int o = 0; o < M / 2 && p == s; ++o) {
+      int r = o;
+      i64 delta = 0;
+#pragma unroll
+      for (int j = D - 1; j >= 0; --j) {
+        delta += (i64)((r % 3) - 1) * (i64)g.stride[j];
+        r /= 3;
+      }
+      u32 ns;
+      if (tab.find(key + (u64)delta, ns) && ns < s) p = ns;
+    }
+    par[s] = p;
     first[s] = 0xffffffffu;
   }
 }
@@ -2178,7 +2196,8 @@ __global__ void k_uf_link(GridParams g, Tab tab, const u32* kp, u32* par) {
         r /= 3;
       }
       u32 ns;
-      if (tab.find(key + (u64)delta, ns)) uf_unite(par, s, ns);
+      if (tab.find(key + (u64)delta, ns) && *(volatile u32*)(par + s) != *(volatile u32*)(par + ns))
+        uf_unite(par, s, ns);
     }
   }
 }
@@ -2189,17 +2208,44 @@ template <int D, class Tab>
 __global__ void k_uf_flatten(Tab tab, const u32* kp, u32* par, Entry<D>* acc) {
   const u32 k = *kp;
   const i64 stride = (i64)gridDim.x * blockDim.x;
-  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
-    const u32 s = tab.list[a];
-    const u32 r = uf_root_ro(par, s);
-    par[s] = r;   // only the owner writes par[s]; every other write is a root
-    const Entry<D>& e = tab.ent[s];
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count (the group sums below are warp collectives)
+  for (i64 base = (i64)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < k; base += stride) {
+    const i64 a = base + lane;
+    u32 r = 0xffffffffu;
+    u64 w[1 + 2 * D];
+#pragma unroll
+    for (int q = 0; q < 1 + 2 * D; ++q) w[q] = 0;
+    if (a < k) {
+      const u32 s = tab.list[a];
+      r = uf_root_ro(par, s);
+      par[s] = r;   // only the owner writes par[s]; every other write is a root
+      const Entry<D>& e = tab.ent[s];
+      w[0] = e.count;
+#pragma unroll
+      for (int j = 0; j < D; ++j) { w[1 + j] = e.hi[j]; w[1 + D + j] = e.lo[j]; }
+    }
+    // cells of one component (most of a warp, for big clusters) add once
+    const unsigned peers = __match_any_sync(kFull, r);
+    if (__any_sync(kFull, __popc(peers) > 1)) {
+#pragma unroll
+      for (int kk = 0; kk < 5; ++kk) {
+        const unsigned src = __fns(peers, lane, (1 << kk) + 1);
+        const int from = src < 32 ? (int)src : lane;
+#pragma unroll
+        for (int q = 0; q < 1 + 2 * D; ++q) {
+          const u64 o = __shfl_sync(kFull, w[q], from);
+          if (src < 32) w[q] += o;
+        }
+      }
+    }
+    if (r == 0xffffffffu || lane != __ffs(peers) - 1) continue;
     Entry<D>* c = acc + r;
-    atomicAdd(&c->count, e.count);
+    atomicAdd(&c->count, w[0]);
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      atomicAdd(&c->hi[j], e.hi[j]);
-      atomicAdd(&c->lo[j], e.lo[j]);
+      atomicAdd(&c->hi[j], w[1 + j]);
+      atomicAdd(&c->lo[j], w[1 + D + j]);
     }
   }
 }
