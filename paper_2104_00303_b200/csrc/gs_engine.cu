@@ -433,7 +433,7 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     launch(c, K_DERIVE, [&] {
       k_derive_brick3<<<nbr, kBrickThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1],
                                                         reinterpret_cast<const Rec<3>*>(rec), ctrl, nby, nbz, bm,
-                                                        occ_cur, occ_nxt, t);
+                                                        occ_cur, occ_nxt, mask + (size_t)cur * nbr * kMaskWords, t);
     });
     bricked = true;
   }

@@ -1263,9 +1263,12 @@ __global__ void __launch_bounds__(kThreads) k_derive(GridParams g, Tab cur, Tab 
 __global__ void __launch_bounds__(kBrickThreads) k_derive_brick3(GridParams g, DenseTable<3> cur, DenseTable<3> nxt,
                                                                  const Rec<3>* __restrict__ rec, Ctrl* ctrl,
                                                                  int nby, int nbz, BrickMap bm, const u8* occ_cur,
-                                                                 u8* occ_nxt, int t) {
+                                                                 u8* occ_nxt, const u32* cmask, int t) {
   if (block_stopped_before(ctrl, t)) return;
   if (!occ_cur[blockIdx.x]) return;
+  // the brick's cell-occupancy mask (written by k_agg_brick3 for this table)
+  // spares the count reads of empty cells
+  const bool mine = (cmask[(size_t)blockIdx.x * kMaskWords + (threadIdx.x >> 5)] >> (threadIdx.x & 31)) & 1u;
   const i64 s0 = (i64)g.stride[0], s1 = (i64)g.stride[1];
   const int ext0 = (int)((i64)g.nkeys / s0), ext1 = (int)(s0 / s1), ext2 = (int)s1;
   const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
@@ -1273,7 +1276,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_derive_brick3(GridParams g, D
   const int z = bz * kBZ + q % kBZ, yv = by * kBY + (q / kBZ) % kBY, x = bx * kBX + q / (kBZ * kBY);
   const bool inside = x < ext0 && yv < ext1 && z < ext2;
   const u32 s = inside ? (u32)(x * s0 + yv * s1 + z) : 0u;
-  const u64 cnt = inside ? cur.ent[s].count : 0;
+  const u64 cnt = (inside && mine) ? cur.ent[s].count : 0;
   u64 key = kEmpty;
   Agg<3> ag;
   ag.zero();
