@@ -525,7 +525,7 @@ void clear_table(gs_ctx* c, const Plan& p, Tab& tab, u32* kp) {
 
 // Extraction of y_final (modeseek.py:256-272).  Table buffer e is clean on
 // entry, buffer e^1 is dirty (cleared here and used as component scratch).
-// `table_ready`: buffer e already holds the table of yf (the last k_step
+// `table_ready`: buffer e already holds the table of yf (the last k_derive
 // built it); otherwise it is clean and gets built here.
 // Phase 1: components of the final table + this process's first-appearance
 // minima (`offset` = global index of its first point, sharded runs).

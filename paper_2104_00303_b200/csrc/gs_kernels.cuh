@@ -448,7 +448,7 @@ __device__ __forceinline__ bool load_quad(const double* __restrict__ y, const Gr
 }
 
 // Histogram of one iterate into a clean table (first iteration, extraction
-// of a user-given point set, table dumps; the loop fuses it into k_step).
+// of a user-given point set, table dumps; the loop derives later tables).
 // Warps take strided super-tiles of kSuper consecutive 128-point tiles, so
 // the grid streams through a narrow window of memory.
 template <int D, class Tab, bool CountOnly = false>
@@ -1403,7 +1403,7 @@ __device__ __forceinline__ void agg_cell(const GridParams& g, const Tab& tab, u3
 // Per occupied cell: 3^d neighbourhood -> target record.  Dense tables are
 // walked slot by slot (empty slots are one 8-byte read); hash tables by
 // their occupied list.  Also clears the previous iteration's table (the
-// next k_step fills it) and records k and the (cells, counts) fingerprint
+// next k_derive fills it) and records k and the (cells, counts) fingerprint
 // of this iteration; the last CTA resets the cleared table's cell count.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab prev, Rec<D>* __restrict__ rec,
@@ -1456,7 +1456,7 @@ __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab pre
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&ctrl->agg_done, 1u) == gridDim.x - 1) {
-      ctrl->k[cur ^ 1] = 0;   // every CTA has read it: the next k_step appends from 0
+      ctrl->k[cur ^ 1] = 0;   // every CTA has read it: the next k_derive appends from 0
       ctrl->agg_done = 0;
     }
   }

@@ -16,6 +16,7 @@ import pytest
 import paper_2104_00303_b200 as gs
 from oracle import gridshift_oracle as O
 from paper_2104_00303_b200 import workloads as W
+from tests import exact_model as X
 from tests import goldens as G
 
 pytestmark = pytest.mark.gpu
@@ -372,3 +373,44 @@ def test_points_api_float32_equals_pointset_upcast():
     bad[3, 1] = np.nan
     with pytest.raises(ValueError):
         gs.meanshiftpp_points(bad, cfg)
+
+
+# ------------------------------------------- streams, in-place accounting
+
+def test_user_stream_and_inplace_accounting():
+    # the engine on a caller's (non-default) stream, with the table chain on
+    # its side stream, gives the identical result; the in-place shift stores
+    # at most the full rewrite, and less once points settle
+    import ctypes as C
+
+    import torch
+
+    from paper_2104_00303_b200 import _lib
+
+    x = W.cloud3d(150_000, seed=61).astype(np.float64)
+    cfg = gs.ShiftConfig(1.0, 1e-3, 25)
+    ref, rtr = gs.meanshiftpp(gs.PointSet(x), cfg)
+    xd = torch.from_numpy(x).cuda()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        lab, k, it, mv, conv = gs.meanshiftpp_device(xd, cfg, stream=st.cuda_stream)
+    st.synchronize()
+    assert np.array_equal(lab.cpu().numpy(), ref.labels) and k == ref.k and it == rtr.iterations
+    np.testing.assert_array_equal(mv, rtr.total_movement_per_iter)
+    wb = np.zeros(it, dtype=np.uint64)
+    _lib.check(_lib.load().gs_fetch_shift_bytes(_lib.context(0), _lib.ptr(wb), C.c_int32(it)))
+    full = 8 * 3 * len(x)
+    # iteration 0 moves nearly every point (isolated background points are
+    # already at their target); no launch stores more than the full rewrite
+    assert wb[0] >= full // 2 and np.all(wb <= full + 64)
+    assert wb[-1] < wb[0]          # settled points are not rewritten
+
+
+def test_points_api_sorted_float64_rows():
+    # the sort reads fp64 host-layout rows directly (SrcAoS<double>)
+    x = W.cloud3d(120_000, seed=62).astype(np.float64)
+    cfg = gs.ShiftConfig(1.0, 1e-3, 15)
+    a, ta = gs.meanshiftpp_points(x, cfg)
+    b = X.meanshiftpp(x, 1.0, 1e-3, 15)
+    assert np.array_equal(a.labels, b["labels"]) and np.array_equal(a.modes, b["modes"])
+    np.testing.assert_array_equal(ta.total_movement_per_iter, b["movement"])
