@@ -109,3 +109,30 @@ def test_invalid_inputs():
         gs.ShiftConfig(h=1.0, max_iters=0)
     with pytest.raises(ValueError):
         gs.meanshiftpp(gs.PointSet(np.zeros((3, 9))), gs.ShiftConfig(1.0))   # d > 8: engine envelope
+
+
+@settings(max_examples=20)
+@given(st.integers(4, 8), st.integers(5, 300), st.sampled_from([0.6, 1.0, 1.7]), st.booleans(),
+       st.integers(0, 2**31 - 1))
+def test_full_run_high_d_bitwise_exact_model(d, n, h, spread, seed):
+    # d = 4..8: dense or hash tables (a wide spread forces the hash path),
+    # k_agg_warp / k_agg, register-prefetched k_shift
+    rng = np.random.default_rng(seed)
+    y = rng.normal(0, 40.0 if spread else 1.2, size=(n, d))
+    lab, tr = gs.meanshiftpp(gs.PointSet(y), gs.ShiftConfig(h=h, max_iters=40))
+    m = X.meanshiftpp(y, h, None, 40)
+    assert tr.iterations == m["iterations"]
+    np.testing.assert_array_equal(tr.total_movement_per_iter, m["movement"])
+    assert np.array_equal(lab.labels, m["labels"]) and np.array_equal(lab.modes, m["modes"])
+
+
+def test_large_hash_run_equals_exact_model():
+    # a sorted (n >= 32768) run on a hash table (d = 4, wide box)
+    rng = np.random.default_rng(77)
+    centers = rng.uniform(-300, 300, size=(12, 4))
+    y = (centers[rng.integers(0, 12, size=60_000)] + rng.normal(0, 1.5, size=(60_000, 4)))
+    lab, tr = gs.meanshiftpp(gs.PointSet(y), gs.ShiftConfig(h=1.0, eta=1e-3, max_iters=30))
+    m = X.meanshiftpp(y, 1.0, 1e-3, 30)
+    assert tr.iterations == m["iterations"]
+    np.testing.assert_array_equal(tr.total_movement_per_iter, m["movement"])
+    assert np.array_equal(lab.labels, m["labels"]) and np.array_equal(lab.modes, m["modes"])
