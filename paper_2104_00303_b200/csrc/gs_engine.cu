@@ -6,6 +6,7 @@
 // chunks and only synchronises between chunks (no per-iteration round trip).
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -138,6 +139,14 @@ void launch(gs_ctx* c, int kind, F&& f) {
   GS_CUDA(cudaEventRecord(prof_event(c), c->st));
   c->prof.rec.emplace_back(kind, i0);
 }
+
+// Kernel attributes (dynamic shared memory limits, carveouts) are set once
+// per device: `done` is a per-call-site bitmask over device ordinals, marked
+// only after the attributes are in place (concurrent first calls both set).
+inline bool attr_pending(const std::atomic<uint64_t>& done, int device) {
+  return (done.load() & (1ull << (device & 63))) == 0;
+}
+inline void attr_done(std::atomic<uint64_t>& done, int device) { done.fetch_or(1ull << (device & 63)); }
 
 inline int blocks_for(gs_ctx* c, int64_t work, int per_sm = 8) {
   const int64_t want = (work + kThreads - 1) / kThreads;
@@ -401,14 +410,14 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     const int nbx = (ext0 + kBX - 1) / kBX, nby = (ext1 + kBY - 1) / kBY, nbz = (ext2 + kBZ - 1) / kBZ;
     const int nbr = nbx * nby * nbz;
     const BrickMap bm{(u32)p.g.stride[0], (u32)p.g.stride[1], (u32)nby, (u32)nbz};
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (attr_pending(attr, c->device)) {
       GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBrickSmem));
       // same (maximal) shared-memory carveout as k_shift_tma, so the chain's
       // CTAs can be co-resident with the shift's on one SM
       GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       GS_CUDA(cudaFuncSetAttribute(k_derive_brick3, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      attr = true;
+      attr_done(attr, c->device);
     }
     u8* occ = ensure<u8>(c, c->bocc, 2 * (size_t)nbr);
     u32* mask = ensure<u32>(c, c->bmask, 2 * (size_t)nbr * kMaskWords);
@@ -457,12 +466,12 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
   if constexpr (Tab::kDense && D <= 3) {
     // bulk-copy pipelined shift: persistent, 2 CTAs per SM
     if (with_shift) {
-      static bool attr = false;
-      if (!attr) {
+      static std::atomic<uint64_t> attr{0};
+      if (attr_pending(attr, c->device)) {
         GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)shift_tma_smem<D>()));
-        attr = true;
+        attr_done(attr, c->device);
       }
       const int64_t ntiles = (n + kShiftTilePts - 1) / kShiftTilePts;
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * 2));
@@ -659,11 +668,11 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
     constexpr int V = SRec<D, RT>::kVec;
     uint4* stage = reinterpret_cast<uint4*>(ensure<double>(c, c->stage, (size_t)n * V * 2));
     const size_t st_smem = bk_stage_smem<D, RT>(nb);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (attr_pending(attr, c->device)) {
       GS_CUDA(cudaFuncSetAttribute(k_bk_stage<D, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_stage_smem<D, RT>(2048)));
       GS_CUDA(cudaFuncSetAttribute(k_bk_tally<D, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTallyWin * 4));
-      attr = true;
+      attr_done(attr, c->device);
     }
     const int nch = (int)((n + kChunkRecs - 1) / kChunkRecs);
     GS_CUDA(cudaMemsetAsync(off, 0, p.slots * sizeof(u32), c->st));
