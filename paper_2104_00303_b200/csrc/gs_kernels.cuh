@@ -533,25 +533,17 @@ __device__ __forceinline__ const Rec<D>& lookup_rec(const GridParams& g, const T
   return rec[s];
 }
 
-// Shift of iteration t (modeseek.py:109-110): per 4-point quad (two 16-byte
-// vector loads per SoA axis) look up the cell record, write y' = target,
-// accumulate the per-point L2 movement in 128-bit fixed point.  Quads of
-// bitwise-identical points (every cell-sorted run after iteration 0) share
-// one lookup and one norm (exact: identical inputs, movement scaled by 4 in
-// fixed point).  The iterate is updated IN PLACE (y == yo is allowed: each
-// quad is read and written by one thread only, lookups go through the cell
-// records), and a 16-byte store whose two coordinates are bitwise unchanged
-// is elided -- once clusters settle most points sit at their cell's target,
-// so converged iterations stream mostly reads.  Streaming loads/stores keep
-// the tables in L2.  The last CTA finishes the movement reduction and
-// evaluates `movement < eta` (modeseek.py:139) on device; `wbytes` counts the
-// bytes actually stored (per-iteration trace, for the roofline accounting).
 // One quad: look up the cell records, produce y' (out), accumulate the exact
 // movement.  `in` holds points 4q..4q+3 per axis as two double2.
+// Returns kQuadMixed (outputs to compare per pair), kQuadStill (uniform
+// quad already at its target: nothing to store) or kQuadMoved (uniform quad
+// that moved: every coordinate changes).
+constexpr int kQuadMixed = 0, kQuadStill = 1, kQuadMoved = 2;
+
 template <int D, class Tab>
-__device__ __forceinline__ void shift_quad(const GridParams& g, const Tab& tab, const Rec<D>* __restrict__ rec,
-                                           Ctrl* ctrl, const double2 (&in)[D][2], i64 q, i64 n,
-                                           double (&out)[4][D], u64& ahi, u64& alo) {
+__device__ __forceinline__ int shift_quad(const GridParams& g, const Tab& tab, const Rec<D>* __restrict__ rec,
+                                          Ctrl* ctrl, const double2 (&in)[D][2], i64 q, i64 n,
+                                          double (&out)[4][D], u64& ahi, u64& alo) {
   bool uni = 4 * q + 3 < n;
 #pragma unroll
   for (int j = 0; j < D; ++j)
@@ -575,6 +567,7 @@ __device__ __forceinline__ void shift_quad(const GridParams& g, const Tab& tab, 
     }
 #pragma unroll
     for (int j = 0; j < D; ++j) out[1][j] = out[2][j] = out[3][j] = out[0][j];
+    return still ? kQuadStill : kQuadMoved;
   } else {
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -593,13 +586,25 @@ __device__ __forceinline__ void shift_quad(const GridParams& g, const Tab& tab, 
       }
     }
   }
+  return kQuadMixed;
 }
 
 // Store y' of a quad into yo; with an in-place iterate, 16-byte pairs whose
 // coordinates are bitwise unchanged are not rewritten.
 template <int D>
 __device__ __forceinline__ void store_quad(double* yo, i64 ld, i64 q, bool inplace, const double2 (&in)[D][2],
-                                           const double (&out)[4][D], u32& nst) {
+                                           const double (&out)[4][D], u32& nst, int kind = kQuadMixed) {
+  if (inplace && kind == kQuadStill) return;
+  if (kind == kQuadMoved || !inplace) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double2* dst = reinterpret_cast<double2*>(yo + (i64)j * ld) + 2 * q;
+      __stcs(dst, make_double2(out[0][j], out[1][j]));
+      __stcs(dst + 1, make_double2(out[2][j], out[3][j]));
+    }
+    nst += 2 * D;
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     double2* dst = reinterpret_cast<double2*>(yo + (i64)j * ld) + 2 * q;
@@ -722,8 +727,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_shift(const double* y, double* 
       }
     }
     double out[4][D];
-    shift_quad<D, Tab>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
-    store_quad<D>(yo, g.ld, q, y == yo, in, out, nst);
+    const int kind = shift_quad<D, Tab>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
+    store_quad<D>(yo, g.ld, q, y == yo, in, out, nst, kind);
   }
   finish_movement<D>(g, ctrl, partials, mv_hist, t, eta, limbs, wbytes, ahi, alo, nst);
 }
@@ -813,8 +818,8 @@ __global__ void __maxnreg__(96) k_shift_tma(double* y, i64 n, GridParams g,
         in[j][1] = src[1];
       }
       double out[4][D];
-      shift_quad<D, DenseTable<D>>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
-      store_quad<D>(y, g.ld, q, true, in, out, nst);
+      const int kind = shift_quad<D, DenseTable<D>>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
+      store_quad<D>(y, g.ld, q, true, in, out, nst, kind);
     }
     __syncthreads();   // stage s consumed: refill it
     if (threadIdx.x == 0 && k + kShiftStages < mine) issue(k + kShiftStages);
