@@ -466,17 +466,20 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
   if constexpr (Tab::kDense && D <= 3) {
     // bulk-copy pipelined shift: persistent, 2 CTAs per SM
     if (with_shift) {
+      // 64-thread CTAs (tile = 256 points), 16 warps per SM: small CTAs
+      // decouple the per-tile barriers (measured 256 -> 64: -1 ms per run)
+      constexpr int T = 64;
       static std::atomic<uint64_t> attr{0};
       if (attr_pending(attr, c->device)) {
-        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)shift_tma_smem<D>()));
+        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)shift_tma_smem<D, T>()));
         attr_done(attr, c->device);
       }
-      const int64_t ntiles = (n + kShiftTilePts - 1) / kShiftTilePts;
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * 2));
+      const int64_t ntiles = (n + 4 * T - 1) / (4 * T);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * 512 / T));
       launch(c, K_SHIFT, [&] {
-        k_shift_tma<D><<<grid, kThreads, shift_tma_smem<D>(), c->st>>>(
+        k_shift_tma<D, T><<<grid, T, shift_tma_smem<D, T>(), c->st>>>(
             y_it, n, p.g, rec, ctrl, static_cast<u64*>(c->partials.p), static_cast<double*>(c->mv_hist.p), t, eta,
             limbs, static_cast<u64*>(c->wr_hist.p) + t);
       });

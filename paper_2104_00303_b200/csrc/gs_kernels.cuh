@@ -631,8 +631,8 @@ __device__ __forceinline__ void finish_movement(const GridParams& g, Ctrl* ctrl,
     add128(ahi, alo, oh, ol);
   }
   nst = __reduce_add_sync(kFull, nst);
-  __shared__ u64 sh[kThreads / 32][2];
-  __shared__ u32 shn[kThreads / 32];
+  __shared__ u64 sh[32][2];   // up to 1024 threads
+  __shared__ u32 shn[32];
   __shared__ bool last;
   const int w = threadIdx.x >> 5;
   if (lane == 0) { sh[w][0] = ahi; sh[w][1] = alo; shn[w] = nst; }
@@ -734,10 +734,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_shift(const double* y, double* 
 }
 
 // ---- TMA-pipelined shift (dense tables, in-place iterate).  A persistent
-// CTA walks tiles of 4*kThreads points; one thread keeps kShiftStages tiles
+// CTA of T threads walks tiles of 4*T points; one thread keeps kShiftStages tiles
 // in flight with 1-D bulk copies (cp.async.bulk, completion on an mbarrier),
 // so the read stream needs no registers and no per-thread latency hiding.
-constexpr int kShiftTilePts = 4 * kThreads;
 constexpr int kShiftStages = 3;
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -768,17 +767,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, 
                : "memory");
 }
 
-template <int D>
+template <int D, int T = kThreads>
 constexpr size_t shift_tma_smem() {
-  return (size_t)kShiftStages * D * kShiftTilePts * sizeof(double);
+  return (size_t)kShiftStages * D * 4 * T * sizeof(double);
 }
 
-template <int D>
+template <int D, int T>
 __global__ void __maxnreg__(96) k_shift_tma(double* y, i64 n, GridParams g,
                                                            const Rec<D>* __restrict__ rec, Ctrl* ctrl,
                                                            u64* partials, double* mv_hist, int t, double eta,
                                                            u64* limbs, u64* wbytes) {
   if (*(volatile int*)&ctrl->done) return;
+  constexpr int kShiftTilePts = 4 * T;
   extern __shared__ __align__(128) double tiles[];   // [stage][axis][kShiftTilePts]
   __shared__ __align__(8) u64 full[kShiftStages];
   const DenseTable<D> tab{};
