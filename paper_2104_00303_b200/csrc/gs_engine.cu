@@ -683,11 +683,12 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
     launch(c, K_SORT, [&] { k_bk_cols<<<nb, 1024, 0, c->st>>>(bk, nblk, nb, btot); });
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(btot, (int)nb); });
     launch(c, K_SORT, [&] { k_bk_stage<D, Src><<<nblk, 512, st_smem, c->st>>>(src, n, shift, nb, chunk, bk, btot, si.cell0, stage); });
-    launch(c, K_SORT, [&] { k_bk_tally<D, RT><<<nch, 512, 2 * kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, si.minidx, ctrl); });
+    launch(c, K_SORT, [&] { k_bk_tally<D, RT><<<nch, kTallyThreads, 2 * kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, si.minidx, ctrl); });
     launch(c, K_SORT, [&] { k_scan_reduce<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, p.slots, off); });
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
     launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, off, p.slots, si.start, off); });
-    launch(c, K_SORT, [&] { k_bk_place<D, RT><<<nch, 512, kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, y1, ctrl); });
+    const int nchp = (int)((n + kRpt * kPlaceThreads - 1) / (kRpt * kPlaceThreads));
+    launch(c, K_SORT, [&] { k_bk_place<D, RT><<<nchp, kPlaceThreads, kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, y1, ctrl); });
     std::swap(c->y[0], c->y[1]);
     // table 0 from the sorted iterate (runs are contiguous: cheap), then the
     // occupied-slot list of the runs

@@ -1788,7 +1788,7 @@ __device__ __forceinline__ void srec_coords(const uint4* rec, double (&v)[D]) {
   for (int j = 0; j < D; ++j) v[j] = (double)c[j];
 }
 
-constexpr int kChunkRecs = 4096;
+constexpr int kChunkRecs = 4096;   // k_bk_tally chunk (k_bk_place uses half)
 constexpr int kBucketShiftMin = 12;        // >= 4096 slots per coarse bucket
 constexpr int kTallyWin = 2 << kBucketShiftMin;   // a chunk spans <= 2 buckets when they are full
 
@@ -1974,18 +1974,21 @@ __global__ void __launch_bounds__(512) k_bk_stage(Src src, i64 n, int shift, u32
   }
 }
 
-// A chunk = kChunkRecs staging records, kRpt per thread of a 512-thread
-// block (record r0 + t*512 + tid); each thread keeps its records' slots and
-// indices in registers across the passes.
-constexpr int kRpt = kChunkRecs / 512;
+// A chunk = TT*kRpt staging records, kRpt per thread of a TT-thread block
+// (record r0 + t*TT + tid); each thread keeps its records' slots and indices
+// in registers across the passes.  k_bk_tally: 512 threads (fewer window
+// clears per record), k_bk_place: 256 threads (shorter barrier chains).
+constexpr int kRpt = 8;
+constexpr int kTallyThreads = 512, kPlaceThreads = 256;
+static_assert(kChunkRecs == kRpt * kTallyThreads, "tally chunk = records per thread x threads");
 
-template <int D, typename RT>
+template <int D, typename RT, int TT>
 __device__ __forceinline__ void load_slots(const uint4* __restrict__ stage, const GridParams& g, i64 r0, i64 r1,
                                            u32 (&key)[kRpt], u32 (&idx)[kRpt], Ctrl* ctrl) {
   constexpr int V = SRec<D, RT>::kVec;
 #pragma unroll
   for (int t = 0; t < kRpt; ++t) {
-    const i64 r = r0 + t * 512 + threadIdx.x;
+    const i64 r = r0 + t * TT + threadIdx.x;
     key[t] = 0xffffffffu;
     idx[t] = 0xffffffffu;
     if (r < r1) {
@@ -2021,7 +2024,7 @@ __device__ __forceinline__ void slots_range(const u32 (&key)[kRpt], u32* kmin_s,
 // shared-memory tallies over the chunk's slot window, then one global atomic
 // pair per (chunk, slot).  cnt must be zero on entry.
 template <int D, typename RT>
-__global__ void __launch_bounds__(512) k_bk_tally(const uint4* __restrict__ stage, i64 n, u64 nslots, GridParams g,
+__global__ void __launch_bounds__(kTallyThreads) k_bk_tally(const uint4* __restrict__ stage, i64 n, u64 nslots, GridParams g,
                                                   u32* cnt, u32* minidx, Ctrl* ctrl) {
   constexpr int WIN = kTallyWin;
   extern __shared__ u32 tsm[];
@@ -2030,7 +2033,7 @@ __global__ void __launch_bounds__(512) k_bk_tally(const uint4* __restrict__ stag
   __shared__ u32 kmin_s, kmax_s;
   const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
   u32 key[kRpt], idx[kRpt];
-  load_slots<D, RT>(stage, g, r0, r1, key, idx, ctrl);
+  load_slots<D, RT, kTallyThreads>(stage, g, r0, r1, key, idx, ctrl);
   slots_range(key, &kmin_s, &kmax_s);
   const u32 kmin = kmin_s;
   const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
@@ -2074,15 +2077,16 @@ __global__ void __launch_bounds__(512) k_bk_tally(const uint4* __restrict__ stag
 // per chunk again: one global cursor bump per (chunk, slot), shared-memory
 // local ranks, SoA fp64 writes of the sorted iterate (off ends as run ends)
 template <int D, typename RT>
-__global__ void __launch_bounds__(512) k_bk_place(const uint4* __restrict__ stage, i64 n, u64 nslots, GridParams g,
+__global__ void __launch_bounds__(kPlaceThreads) k_bk_place(const uint4* __restrict__ stage, i64 n, u64 nslots, GridParams g,
                                                   u32* off, double* __restrict__ ys, Ctrl* ctrl) {
   constexpr int WIN = kTallyWin;
   constexpr int V = SRec<D, RT>::kVec;
   extern __shared__ u32 cnt[];
   __shared__ u32 kmin_s, kmax_s;
-  const i64 r0 = (i64)blockIdx.x * kChunkRecs, r1 = min(n, r0 + kChunkRecs);
+  constexpr i64 kPlaceRecs = (i64)kRpt * kPlaceThreads;
+  const i64 r0 = (i64)blockIdx.x * kPlaceRecs, r1 = min(n, r0 + kPlaceRecs);
   u32 key[kRpt], idx[kRpt];
-  load_slots<D, RT>(stage, g, r0, r1, key, idx, ctrl);
+  load_slots<D, RT, kPlaceThreads>(stage, g, r0, r1, key, idx, ctrl);
   slots_range(key, &kmin_s, &kmax_s);
   const u32 kmin = kmin_s;
   const bool wide = kmax_s >= nslots || kmax_s - kmin >= (u32)WIN;
@@ -2111,7 +2115,7 @@ __global__ void __launch_bounds__(512) k_bk_place(const uint4* __restrict__ stag
   for (int t = 0; t < kRpt; ++t) {
     if (key[t] == 0xffffffffu || pos[t] >= (u32)n) continue;
     double v[D];
-    srec_coords<D, RT>(stage + (r0 + t * 512 + threadIdx.x) * V, v);
+    srec_coords<D, RT>(stage + (r0 + t * kPlaceThreads + threadIdx.x) * V, v);
 #pragma unroll
     for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * g.ld + pos[t], v[j]);
   }
