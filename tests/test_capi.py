@@ -69,3 +69,30 @@ def test_library_is_sm100a_code():
 def test_null_context_is_rejected(lib):
     rc = lib.gs_meanshiftpp(None, None, 1, 1, 1.0, 1.0, 1, None, None, None, None, None)
     assert rc == _lib.GS_EINVAL
+
+
+def _build_c_host(tmp_path):
+    exe = tmp_path / "c_host"
+    libdir = ROOT / "paper_2104_00303_b200"
+    subprocess.run(["gcc", "-O2", "-I", str(ROOT / "include"), str(ROOT / "examples" / "c_host.c"),
+                    "-L", str(libdir), "-lgridshift_cuda", f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)],
+                   check=True)
+    return exe
+
+
+def test_c_host_links_against_the_header_and_library(lib, tmp_path):
+    # a plain C caller (no Python): compiles against include/gridshift_cuda.h,
+    # links libgridshift_cuda.so and loads it (no GPU needed for --version)
+    exe = _build_c_host(tmp_path)
+    out = subprocess.run([str(exe), "--version"], capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.gpu
+def test_c_host_runs_the_engine(lib, tmp_path):
+    exe = _build_c_host(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert "k=2 " in out and "converged=1" in out
+    modes = sorted(tuple(float(v) for v in line.split("(")[1].rstrip(")").split(","))
+                   for line in out.splitlines() if line.startswith("mode "))
+    assert abs(modes[0][0] - 2.0) < 0.05 and abs(modes[1][0] - 8.0) < 0.05
