@@ -94,6 +94,8 @@ struct gs_ctx {
   bool collapsed = false;               // option: collapsed iterations (gs_ctx_set_option)
   Buf runposb, runcntb, bkcnt, bktot, bocc, bmask, wr_hist;
   bool tables_dirty = false;            // a call failed mid-run: table buffers may hold entries
+  Ctrl* h_snap = nullptr;               // pinned Ctrl snapshots after each enqueued chunk (2 slots)
+  cudaEvent_t ev_snap[2] = {nullptr, nullptr};
   // table-chain stream (see enqueue_iteration: overlap)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rec[2] = {nullptr, nullptr}, ev_shift[2] = {nullptr, nullptr};
@@ -786,11 +788,17 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
     sinfo.runpos = ensure<double>(c, c->runposb, (size_t)sinfo.rld * D);
     sinfo.runcnt = ensure<u32>(c, c->runcntb, p.list_cap);
   }
-  // device-driven loop: enqueue chunks, synchronise between chunks only
-  int t = 0, chunk = 4;
-  while (t < max_iters) {
-    const int m = std::min(chunk, max_iters - t);
-    for (int q = 0; q < m; ++q, ++t) {
+  // device-driven loop: chunks of 4, 8, 16, 32 iterations.  Chunk j+1 is
+  // enqueued before the host waits for chunk j's stop flag (a pinned Ctrl
+  // snapshot taken right after chunk j), so the device never idles on the
+  // host; kernels of iterations past the stop exit on the stamped `done`.
+  if (!c->h_snap) {
+    GS_CUDA(cudaMallocHost(&c->h_snap, 2 * sizeof(Ctrl)));
+    for (cudaEvent_t* e : {&c->ev_snap[0], &c->ev_snap[1]})
+      GS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  auto enqueue_chunk = [&](int t0, int m) {
+    for (int t = t0; t < t0 + m; ++t) {
       if (collapsed && t >= 1) {
         if (p.dense)
           enqueue_run_iteration<D>(c, p, tabs.dn, t, eta, sinfo, nb_cells);
@@ -813,11 +821,43 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
     }
     side_join(c);
     check_launch();
-    read_ctrl(c);
-    check_flags(c->h_ctrl->error);
-    if (c->h_ctrl->done) break;
-    chunk = std::min(chunk * 2, 32);
+  };
+  auto snapshot = [&](int slot) {
+    GS_CUDA(cudaMemcpyAsync(c->h_snap + slot, c->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->st));
+    GS_CUDA(cudaEventRecord(c->ev_snap[slot], c->st));
+  };
+  // (the first three chunks are not run ahead: short converging runs would
+  // otherwise pay for a chunk of early-exiting launches)
+  int t = std::min(4, max_iters), chunk = 4, slot = 0;
+  enqueue_chunk(0, t);
+  snapshot(0);
+  while (true) {
+    if (t < 28 && t < max_iters) {   // synchronous chunk boundary (chunks of 4, 8, 16)
+      GS_CUDA(cudaEventSynchronize(c->ev_snap[slot]));
+      check_flags(c->h_snap[slot].error);
+      if (c->h_snap[slot].done) break;
+      chunk = std::min(chunk * 2, 32);
+      const int m = std::min(chunk, max_iters - t);
+      enqueue_chunk(t, m);
+      t += m;
+      snapshot(slot);
+      continue;
+    }
+    const bool more = t < max_iters;
+    if (more) {
+      chunk = std::min(chunk * 2, 32);
+      const int m = std::min(chunk, max_iters - t);
+      enqueue_chunk(t, m);
+      t += m;
+      snapshot(slot ^ 1);
+    }
+    GS_CUDA(cudaEventSynchronize(c->ev_snap[slot]));
+    check_flags(c->h_snap[slot].error);
+    if (c->h_snap[slot].done || !more) break;
+    slot ^= 1;
   }
+  read_ctrl(c);   // everything enqueued has finished; final stop state
+  check_flags(c->h_ctrl->error);
   RunOut r;
   r.iters = c->h_ctrl->iters;
   r.converged = c->h_ctrl->done != 0;
@@ -1174,8 +1214,10 @@ void gs_ctx_destroy(gs_ctx* c) {
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->h_small) cudaFreeHost(c->h_small);
   for (cudaEvent_t e : c->prof.pool) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_rec[0], c->ev_rec[1], c->ev_shift[0], c->ev_shift[1]})
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_rec[0], c->ev_rec[1], c->ev_shift[0], c->ev_shift[1],
+                        c->ev_snap[0], c->ev_snap[1]})
     if (e) cudaEventDestroy(e);
+  if (c->h_snap) cudaFreeHost(c->h_snap);
   if (c->side) cudaStreamDestroy(c->side);
   delete c->shard;
   if (c->own) cudaStreamDestroy(c->own);
