@@ -99,6 +99,7 @@ struct gs_ctx {
   // table-chain stream (see enqueue_iteration: overlap)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rec[2] = {nullptr, nullptr}, ev_shift[2] = {nullptr, nullptr};
+  cudaEvent_t ev_pace[2] = {nullptr, nullptr};   // timing-enabled, around side-stream kernels
   struct ShardState* shard = nullptr;   // row-sharded run in progress (gs_shard_*)
 };
 
@@ -132,7 +133,14 @@ template <typename F>
 void launch(gs_ctx* c, int kind, F&& f) {
   c->prof.launches[kind] += 1;
   if (!c->prof.on) {
+    // side-stream kernels are bracketed by timing-enabled events: measured
+    // 37.7 -> 34.7 ms per 100M-point run against no events (or events
+    // without timing), with identical results -- it changes how the
+    // low-priority table chain is scheduled next to the shift
+    const bool pace = c->side && c->st == c->side;
+    if (pace) GS_CUDA(cudaEventRecord(c->ev_pace[0], c->st));
     f();
+    if (pace) GS_CUDA(cudaEventRecord(c->ev_pace[1], c->st));
     return;
   }
   const size_t i0 = c->prof.used;
@@ -371,6 +379,7 @@ void side_init(gs_ctx* c) {
   GS_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, least));
   for (cudaEvent_t* e : {&c->ev_fork, &c->ev_join, &c->ev_rec[0], &c->ev_rec[1], &c->ev_shift[0], &c->ev_shift[1]})
     GS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&c->ev_pace[0], &c->ev_pace[1]}) GS_CUDA(cudaEventCreate(e));
 }
 
 // main stream waits for everything enqueued on the side stream so far
@@ -1215,7 +1224,7 @@ void gs_ctx_destroy(gs_ctx* c) {
   if (c->h_small) cudaFreeHost(c->h_small);
   for (cudaEvent_t e : c->prof.pool) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_rec[0], c->ev_rec[1], c->ev_shift[0], c->ev_shift[1],
-                        c->ev_snap[0], c->ev_snap[1]})
+                        c->ev_snap[0], c->ev_snap[1], c->ev_pace[0], c->ev_pace[1]})
     if (e) cudaEventDestroy(e);
   if (c->h_snap) cudaFreeHost(c->h_snap);
   if (c->side) cudaStreamDestroy(c->side);
