@@ -297,6 +297,18 @@ struct Agg {
     }
     return r;
   }
+  // butterfly sum over the warp (every lane ends with the total)
+  __device__ __forceinline__ void warp_sum() {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      cnt += __shfl_xor_sync(kFull, cnt, off);
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        hi[j] += (i64)__shfl_xor_sync(kFull, (unsigned long long)hi[j], off);
+        lo[j] += __shfl_xor_sync(kFull, lo[j], off);
+      }
+    }
+  }
 };
 
 // Flush one finished segment (a run of points with the same cell key).
@@ -421,6 +433,9 @@ __device__ __forceinline__ void rbk_tile(const GridParams& g, const Tab& tab, Ct
 #define GS_HIST_S 8
 #endif
 constexpr int kSuper = GS_HIST_S;   // tiles per warp super-tile
+#ifndef GS_HIST_PF
+#define GS_HIST_PF 1
+#endif
 
 // Load a lane's 4 consecutive points of tile starting at i0 (SoA, 16-byte
 // vector loads) and classify: `uni` = the lane's 4 points are bitwise
@@ -466,9 +481,21 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(
     u64 ckey = kEmpty;
     Agg<D> cagg;
     cagg.zero();
+    // dist: the carry is spread over the lanes (its value is the sum of the
+    // lanes' cagg) -- key-uniform tiles (all 128 points in the open cell, the
+    // common case on a cell-sorted iterate) add into it lane-privately, with
+    // no shuffles; it is folded back before anything reads it
+    bool dist = false;
     const i64 t_end = min(ntiles, (sup + 1) * kSuper);
     for (i64 tile = sup * kSuper; tile < t_end; ++tile) {
       const i64 i0 = tile * TILE + P * lane;
+      if (GS_HIST_PF > 0 && tile + GS_HIST_PF < t_end) {
+        // L2 prefetch GS_HIST_PF tiles ahead: the next loads of this warp
+        // hit L2 instead of waiting the full HBM latency
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(y + (i64)j * g.ld + i0 + GS_HIST_PF * TILE));
+      }
       double v[P][D];
       bool uni;
       const bool tu = load_quad<D>(y, g, i0, n, v, uni);
@@ -493,8 +520,30 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(
           }
         }
       }
+      if (!tu) {
+        bool ku = valid[P - 1] & (key[0] != kEmpty);
+#pragma unroll
+        for (int m = 1; m < P; ++m) ku &= key[m] == key[0];
+        ku &= __shfl_sync(kFull, key[0], 0) == key[0];
+        if (__all_sync(kFull, ku)) {
+          if (key[0] != ckey) {
+            if (dist) cagg.warp_sum();
+            if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
+            ckey = key[0];
+            cagg.zero();
+          } else if (!dist && lane) {
+            cagg.zero();   // lane 0 keeps the (uniform) carry
+          }
+          dist = true;
+#pragma unroll
+          for (int m = 0; m < P; ++m) cagg.add(item_of<D, CountOnly>(g, v[m], true));
+          continue;
+        }
+      }
+      if (dist) { cagg.warp_sum(); dist = false; }
       rbk_tile<D, Tab, CountOnly>(g, tab, ctrl, lane, key, v, valid, tu, ckey, cagg);
     }
+    if (dist) cagg.warp_sum();
     if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
   }
 }
