@@ -437,8 +437,21 @@ def e2e(x_host, cfg, n, steps):
         ups += n * tr.iterations
         k = lab.k
     dt = time.perf_counter() - t0
-    return {"value": ups / dt, "unit": UNIT, "h2d_bytes_per_step": int(pts.nbytes),
-            "d2h_bytes_per_step": int(lab_out.nbytes + k * 3 * 8), "steps": steps,
+    # bytes the last call moved, as the library counted them: the fp32 rows
+    # up; down the per-point initial-cell index (copied while the loop runs)
+    # + per-cell labels, expanded into lab_out by host threads (sorted dense
+    # path), or the int64 labels otherwise; + the modes
+    import ctypes as C
+
+    from paper_2104_00303_b200 import _lib
+
+    hb, db = C.c_int64(0), C.c_int64(0)
+    _lib.check(_lib.load().gs_fetch_transfer_bytes(_lib.context(), _lib.ref(hb), _lib.ref(db)))
+    assert hb.value == pts.nbytes, (hb.value, pts.nbytes)
+    return {"value": ups / dt, "unit": UNIT, "h2d_bytes_per_step": int(hb.value),
+            "d2h_bytes_per_step": int(db.value), "steps": steps,
+            "labels": "int64 into the caller's pinned buffer; the sorted dense path sends 4 B/point of "
+                      "initial-cell index during the loop + 4 B/cell of labels and expands on the host",
             "api": "paper_2104_00303_b200.meanshiftpp_points(float32 (n,3), ShiftConfig) -> "
                    "gs_meanshiftpp_host (C ABI)"}
 

@@ -132,6 +132,13 @@ GS_API int gs_fetch_trace(gs_ctx* ctx, int64_t* k_per_iter, uint64_t* fp_per_ite
  * rewritten; reads are always 8*d bytes per point).  Roofline accounting. */
 GS_API int gs_fetch_shift_bytes(gs_ctx* ctx, uint64_t* bytes_per_iter, int32_t cap);
 
+/* Host<->device bytes of the last host entry point call (gs_meanshiftpp,
+ * gs_meanshiftpp_host, gs_segment_image): the input upload, and the label
+ * delivery -- either 8 bytes per point, or on the sorted dense path 4 bytes
+ * per point (initial-cell index, copied while the loop runs) plus 4 bytes per
+ * lattice cell (per-cell labels) -- plus the modes.  End-to-end accounting. */
+GS_API int gs_fetch_transfer_bytes(gs_ctx* ctx, int64_t* h2d_bytes, int64_t* d2h_bytes);
+
 /* Kernel accounting.  mode 1: enable per-launch CUDA-event timing (and
  * reset counters); mode 0: disable (and reset); mode 2: write the
  * accumulated device milliseconds and launch counts per kernel kind

@@ -42,6 +42,7 @@ SIGNATURES = {
     "gs_ctx_set_option": (C.c_int, [_P, _i32, _i64]),
     "gs_fetch_trace": (C.c_int, [_P, _P, _P, _i32]),
     "gs_fetch_shift_bytes": (C.c_int, [_P, _P, _i32]),
+    "gs_fetch_transfer_bytes": (C.c_int, [_P, _P, _P]),
     "gs_profile": (C.c_int, [_P, _i32, _P, _P, _i32]),
     "gs_profile_kind": (C.c_char_p, [_i32]),
     "gs_shift_step": (C.c_int, [_P, _P, _i64, _i32, _f64, _P, _P]),

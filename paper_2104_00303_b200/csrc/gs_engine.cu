@@ -14,7 +14,12 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <chrono>
+#include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "../../include/gridshift_cuda.h"
 #include "gs_kernels.cuh"
@@ -101,6 +106,24 @@ struct gs_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rec[2] = {nullptr, nullptr}, ev_shift[2] = {nullptr, nullptr};
   cudaEvent_t ev_pace[2] = {nullptr, nullptr};   // timing-enabled, around side-stream kernels
   struct ShardState* shard = nullptr;   // row-sharded run in progress (gs_shard_*)
+  // host label delivery (sorted runs through the host entry points): the
+  // per-point initial-cell index is copied to the host on `copy` while the
+  // loop runs; the extraction then sends per-cell labels only and the host
+  // expands them (deliver_labels)
+  bool host_labels = false;             // request, set by the host entry points
+  bool cell0_pending = false;           // the cell0 copy is enqueued (on `copy`)
+  bool labels_on_host = false;          // extraction left per-cell labels in h_slotlab
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_sorted = nullptr, ev_cell0 = nullptr;
+  u32* h_cell0 = nullptr;               // pinned, n entries
+  size_t h_cell0_cap = 0;
+  u32* h_slotlab = nullptr;             // pinned, per initial slot: label rank
+  size_t h_slotlab_cap = 0;
+  Buf slotlab;
+  const u32* cell0_dev = nullptr;
+  int64_t cell0_n = 0;
+  int64_t xfer_h2d = 0, xfer_d2h = 0;   // last host call (gs_fetch_transfer_bytes)
+  size_t slotlab_bytes = 0;
 };
 
 namespace {
@@ -349,6 +372,7 @@ struct SortInfo {
   u32* runs = nullptr;      // occupied initial slots
   u32* runroot = nullptr;   // per initial slot: final component root (scratch)
   u32* end = nullptr;       // per initial slot: run end (the scatter cursors)
+  uint64_t slots0 = 0;      // table slots at sort time (the range of cell0)
   double* runpos = nullptr; // collapsed mode: per-run positions (SoA, ld = rld)
   u32* runcnt = nullptr;
   int64_t rld = 0;
@@ -388,6 +412,121 @@ void side_join(gs_ctx* c) {
   GS_CUDA(cudaEventRecord(c->ev_join, c->side));
   GS_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
 }
+
+// ------------------------------------------------- host label delivery
+// A host caller wants labels[i] (int64, original order) in host memory.
+// On the sorted dense path the label of point i is a function of its
+// initial cell alone (labels = rank[root[cell0[i]]], k_labels_runs), and
+// cell0 is final right after the spatial sort.  So the 4-byte cell0 array
+// crosses PCIe while the loop runs (copy stream), the extraction sends the
+// per-cell labels (4 bytes per table slot) instead of 8 bytes per point,
+// and the host expands them.  Same values as k_labels_runs + a D2H copy.
+
+// after the sort was enqueued on c->st: remember where cell0 is
+void cell0_mark(gs_ctx* c, const u32* cell0, int64_t n) {
+  if (!c->copy) {
+    GS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    GS_CUDA(cudaEventCreateWithFlags(&c->ev_sorted, cudaEventDisableTiming));
+    GS_CUDA(cudaEventCreateWithFlags(&c->ev_cell0, cudaEventDisableTiming));
+  }
+  if (c->h_cell0_cap < (size_t)n) {
+    if (c->h_cell0) GS_CUDA(cudaFreeHost(c->h_cell0));
+    c->h_cell0 = nullptr;
+    c->h_cell0_cap = 0;
+    GS_CUDA(cudaMallocHost(&c->h_cell0, sizeof(u32) * (size_t)n));
+    c->h_cell0_cap = (size_t)n;
+  }
+  GS_CUDA(cudaEventRecord(c->ev_sorted, c->st));
+  c->cell0_dev = cell0;
+  c->cell0_n = n;
+}
+
+// issue the cell0 copy.  Called once the host has run-ahead chunks in
+// flight (or after the loop): the synchronous chunk boundaries read small
+// Ctrl snapshots device->host, which must not queue behind a large copy.
+void cell0_copy_start(gs_ctx* c) {
+  if (!c->cell0_dev || c->cell0_pending) return;
+  GS_CUDA(cudaStreamWaitEvent(c->copy, c->ev_sorted, 0));
+  GS_CUDA(cudaMemcpyAsync(c->h_cell0, c->cell0_dev, sizeof(u32) * (size_t)c->cell0_n, cudaMemcpyDeviceToHost,
+                          c->copy));
+  GS_CUDA(cudaEventRecord(c->ev_cell0, c->copy));
+  c->cell0_pending = true;
+}
+
+inline int64_t label_of(u32 s, const u32* lab) { return s == 0xffffffffu ? -1 : (int64_t)lab[s]; }
+
+#if defined(__x86_64__)
+// 16 points per step: gather the cell labels, widen, streaming stores (the
+// output is written once and not read back here)
+__attribute__((target("avx512f"))) void expand_avx512(const u32* c0, const u32* lab, int64_t a, int64_t b,
+                                                       int64_t* out) {
+  int64_t i = a;
+  for (; i < b && ((uintptr_t)(out + i) & 63); ++i) out[i] = label_of(c0[i], lab);
+  const __m512i none = _mm512_set1_epi32(-1);
+  const __m512i neg = _mm512_set1_epi64(-1);
+  for (; i + 16 <= b; i += 16) {
+    const __m512i s = _mm512_loadu_si512(c0 + i);
+    const __mmask16 ok = _mm512_cmpneq_epu32_mask(s, none);
+    const __m512i v = _mm512_mask_i32gather_epi32(none, ok, s, lab, 4);
+    const __m512i lo = _mm512_mask_mov_epi64(neg, (__mmask8)ok, _mm512_cvtepu32_epi64(_mm512_castsi512_si256(v)));
+    const __m512i hi =
+        _mm512_mask_mov_epi64(neg, (__mmask8)(ok >> 8), _mm512_cvtepu32_epi64(_mm512_extracti64x4_epi64(v, 1)));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(out + i), lo);
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(out + i + 8), hi);
+  }
+  for (; i < b; ++i) out[i] = label_of(c0[i], lab);
+  _mm_sfence();
+}
+#endif
+
+// labels[i] = lab[c0[i]] over host threads
+void expand_labels(const u32* c0, const u32* lab, int64_t n, int64_t* out) {
+  unsigned T = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < (int64_t)1 << 20) T = 1;
+#if defined(__x86_64__)
+  const bool avx = __builtin_cpu_supports("avx512f");
+#endif
+  auto work = [&](unsigned t) {
+    const int64_t a = (n * t / T) & ~int64_t(7), b = t + 1 == T ? n : (n * (t + 1) / T) & ~int64_t(7);
+#if defined(__x86_64__)
+    if (avx) { expand_avx512(c0, lab, a, b, out); return; }
+#endif
+    for (int64_t i = a; i < b; ++i) out[i] = label_of(c0[i], lab);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < T; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (std::thread& th : pool) th.join();
+}
+
+// the end of a host entry point: labels into the caller's host buffer
+void deliver_labels(gs_ctx* c, const int64_t* dl, int64_t* out, int64_t n) {
+  if (c->labels_on_host) {
+    static const bool dbg = getenv("GS_DEBUG_DELIVERY") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t0 = now();
+    GS_CUDA(cudaEventSynchronize(c->ev_cell0));
+    sync(c);
+    const double t1 = now();
+    expand_labels(c->h_cell0, c->h_slotlab, n, out);
+    c->xfer_d2h = (int64_t)sizeof(u32) * n + (int64_t)c->slotlab_bytes;
+    if (dbg) fprintf(stderr, "deliver: wait %.3f ms expand %.3f ms\n", t1 - t0, now() - t1);
+  } else {
+    GS_CUDA(cudaMemcpyAsync(out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    c->xfer_d2h = (int64_t)sizeof(int64_t) * n;
+  }
+  c->xfer_d2h += (int64_t)(c->modes_host.size() * sizeof(double));
+  c->labels_on_host = false;
+  c->cell0_pending = false;
+}
+
+// set for the duration of a host entry point's engine run
+struct HostLabelRequest {
+  gs_ctx* c;
+  explicit HostLabelRequest(gs_ctx* cc) : c(cc) { c->host_labels = true; }
+  ~HostLabelRequest() { c->host_labels = false; }
+};
 
 // Iteration t: table t (buffer t&1) holds the cells of y_t.  k_agg turns it
 // into per-cell target records (and clears buffer (t+1)&1), k_derive builds
@@ -620,7 +759,21 @@ void extract_finish(gs_ctx* c, const Plan& p, Tab* tabs, const double* yf, int64
   GS_CUDA(cudaMemcpyAsync(dranks, rk.data(), nr * sizeof(u32), cudaMemcpyHostToDevice, c->st));
   double* dmodes = ensure<double>(c, c->modes, (size_t)nr * D + 1);
   launch(c, K_COMP, [&] { k_modes<D><<<blocks_for(c, nr), kThreads, 0, c->st>>>(p.g, roots, dranks, nr, rankmap, tabs[e ^ 1].ent, dmodes); });
-  if (si)
+  if (si && c->host_labels && c->cell0_pending && Tab::kDense) {
+    // host delivery: per-cell labels only (see deliver_labels)
+    u32* sl = ensure<u32>(c, c->slotlab, si->slots0);
+    launch(c, K_LABELS, [&] { k_slot_labels<<<nb_cells, kThreads, 0, c->st>>>(si->runs, &ctrl->nruns, si->runroot, rankmap, sl); });
+    if (c->h_slotlab_cap < si->slots0) {
+      if (c->h_slotlab) GS_CUDA(cudaFreeHost(c->h_slotlab));
+      c->h_slotlab = nullptr;
+      c->h_slotlab_cap = 0;
+      GS_CUDA(cudaMallocHost(&c->h_slotlab, sizeof(u32) * si->slots0));
+      c->h_slotlab_cap = si->slots0;
+    }
+    GS_CUDA(cudaMemcpyAsync(c->h_slotlab, sl, sizeof(u32) * si->slots0, cudaMemcpyDeviceToHost, c->st));
+    c->slotlab_bytes = sizeof(u32) * si->slots0;
+    c->labels_on_host = true;
+  } else if (si)
     launch(c, K_LABELS, [&] {
       k_labels_runs<<<nb_pts, kThreads, 0, c->st>>>(si->cell0, n, si->runroot, rankmap, reinterpret_cast<i64*>(labels_dev));
     });
@@ -663,6 +816,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
   si.minidx = ensure<u32>(c, c->runmin, p.slots);
   si.runs = ensure<u32>(c, c->runlist, p.list_cap);
   si.cell0 = ensure<u32>(c, c->cell0, (size_t)n);
+  si.slots0 = p.slots;
   si.runroot = off;   // the cursors are dead once the scatter is done...
   si.end = off;       // ...except as run ends, read (collapsed mode) before runroot is written
   GS_CUDA(cudaMemsetAsync(si.minidx, 0xff, p.slots * sizeof(u32), c->st));
@@ -736,6 +890,11 @@ struct RunOut {
 template <int D>
 RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta, int max_iters,
                     int64_t* labels_dev, double* movement_out) {
+  // a cell0 copy of an earlier (failed) call may still read the buffer
+  if (c->copy) GS_CUDA(cudaStreamWaitEvent(c->st, c->ev_cell0, 0));
+  c->cell0_dev = nullptr;
+  c->cell0_pending = false;
+  c->labels_on_host = false;
   double* y0 = ensure<double>(c, c->y[0], (size_t)soa_ld(n) * D);
   ensure<double>(c, c->y[1], (size_t)soa_ld(n) * D);
   ensure<Ctrl>(c, c->ctrl, 1);
@@ -769,6 +928,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
     table0 = spatial_sort<D>(c, p, tabs.dn, n, sinfo, SrcAoS<D, double>{static_cast<const double*>(in.dev)});
   else if (sorted)
     table0 = spatial_sort<D>(c, p, tabs.dn, n, sinfo, soa);
+  if (sorted && p.dense && c->host_labels) cell0_mark(c, sinfo.cell0, n);
   if (sorted && !p.dense) {
     // k never grows (k_{t+1} <= k_t: y_{t+1} takes at most k_t distinct
     // values), so the loop's hash tables only need 2*k_0 slots: compact
@@ -859,12 +1019,14 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
       enqueue_chunk(t, m);
       t += m;
       snapshot(slot ^ 1);
+      cell0_copy_start(c);
     }
     GS_CUDA(cudaEventSynchronize(c->ev_snap[slot]));
     check_flags(c->h_snap[slot].error);
     if (c->h_snap[slot].done || !more) break;
     slot ^= 1;
   }
+  cell0_copy_start(c);
   read_ctrl(c);   // everything enqueued has finished; final stop state
   check_flags(c->h_ctrl->error);
   RunOut r;
@@ -1228,6 +1390,13 @@ void gs_ctx_destroy(gs_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->h_snap) cudaFreeHost(c->h_snap);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->copy) cudaStreamSynchronize(c->copy);
+  if (c->h_cell0) cudaFreeHost(c->h_cell0);
+  if (c->h_slotlab) cudaFreeHost(c->h_slotlab);
+  if (c->slotlab.p) cudaFree(c->slotlab.p);
+  for (cudaEvent_t e : {c->ev_sorted, c->ev_cell0})
+    if (e) cudaEventDestroy(e);
+  if (c->copy) cudaStreamDestroy(c->copy);
   delete c->shard;
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
@@ -1240,11 +1409,15 @@ int gs_meanshiftpp(gs_ctx* c, const double* x, int64_t n, int32_t d, double h, d
     validate_run(n, d, h, eta, max_iters);
     if (!x || !labels_out) fail(GS_EINVAL, "null buffer");
     const double* dx = stage_input(c, x, n, d);
+    c->xfer_h2d = (int64_t)sizeof(double) * n * d;
     int64_t* dl = ensure<int64_t>(c, c->labels, n);
     Input in{IN_F64, dx};
-    RunOut r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
-    GS_CUDA(cudaMemcpyAsync(labels_out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
+    RunOut r;
+    {
+      HostLabelRequest req(c);
+      r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
+    }
+    deliver_labels(c, dl, labels_out, n);
     if (k_out) *k_out = r.k;
     if (iters_out) *iters_out = r.iters;
     if (converged_out) *converged_out = r.converged;
@@ -1261,11 +1434,15 @@ int gs_meanshiftpp_host(gs_ctx* c, const void* x, int32_t dtype, int64_t n, int3
     const size_t esz = dtype == GS_DTYPE_F64 ? 8 : 4;
     unsigned char* dx = ensure<unsigned char>(c, c->x_stage, (size_t)n * d * esz);
     GS_CUDA(cudaMemcpyAsync(dx, x, (size_t)n * d * esz, cudaMemcpyHostToDevice, c->st));
+    c->xfer_h2d = (int64_t)(n * d * esz);
     int64_t* dl = ensure<int64_t>(c, c->labels, n);
     Input in{dtype == GS_DTYPE_F64 ? IN_F64 : IN_F32, dx};
-    RunOut r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
-    GS_CUDA(cudaMemcpyAsync(labels_out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
+    RunOut r;
+    {
+      HostLabelRequest req(c);
+      r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
+    }
+    deliver_labels(c, dl, labels_out, n);
     if (k_out) *k_out = r.k;
     if (iters_out) *iters_out = r.iters;
     if (converged_out) *converged_out = r.converged;
@@ -1301,11 +1478,15 @@ int gs_segment_image(gs_ctx* c, const uint8_t* pixels, int32_t height, int32_t w
     if (!std::isfinite(scale)) fail(GS_EINVAL, "point data contains NaN or infinite entries");
     unsigned char* dp = ensure<unsigned char>(c, c->x_stage, (size_t)n * 3);
     GS_CUDA(cudaMemcpyAsync(dp, pixels, (size_t)n * 3, cudaMemcpyHostToDevice, c->st));
+    c->xfer_h2d = n * 3;
     int64_t* dl = ensure<int64_t>(c, c->labels, n);
     Input in{IN_IMAGE, dp, width, scale};
-    RunOut r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
-    GS_CUDA(cudaMemcpyAsync(labels_out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
+    RunOut r;
+    {
+      HostLabelRequest req(c);
+      r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
+    }
+    deliver_labels(c, dl, labels_out, n);
     if (k_out) *k_out = r.k;
     if (iters_out) *iters_out = r.iters;
     if (converged_out) *converged_out = r.converged;
@@ -1373,6 +1554,13 @@ int gs_fetch_shift_bytes(gs_ctx* c, uint64_t* bytes_per_iter, int32_t cap) {
       GS_CUDA(cudaMemcpyAsync(bytes_per_iter, c->wr_hist.p, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost, c->st));
       sync(c);
     }
+  });
+}
+
+int gs_fetch_transfer_bytes(gs_ctx* c, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+  return guarded(c, [&] {
+    if (h2d_bytes) *h2d_bytes = c->xfer_h2d;
+    if (d2h_bytes) *d2h_bytes = c->xfer_d2h;
   });
 }
 

@@ -1734,6 +1734,19 @@ __global__ void k_run_first(const double* __restrict__ yf, GridParams g, Tab tab
   }
 }
 
+// per-cell labels of the initial cells (host delivery: the host expands
+// them through its copy of cell0; k_labels_runs's values)
+__global__ void __launch_bounds__(kThreads) k_slot_labels(const u32* __restrict__ runs, const u32* nruns,
+                                                          const u32* __restrict__ runroot,
+                                                          const u32* __restrict__ rankmap, u32* slotlab) {
+  const u32 R = *nruns;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < R; a += stride) {
+    const u32 s0 = runs[a];
+    slotlab[s0] = rankmap[runroot[s0]];
+  }
+}
+
 // labels in original order: one coalesced pass (cell0 -> run root -> rank)
 __global__ void __launch_bounds__(kThreads) k_labels_runs(const u32* __restrict__ cell0, i64 n,
                                                           const u32* __restrict__ runroot,

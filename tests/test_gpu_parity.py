@@ -414,3 +414,34 @@ def test_points_api_sorted_float64_rows():
     b = X.meanshiftpp(x, 1.0, 1e-3, 15)
     assert np.array_equal(a.labels, b["labels"]) and np.array_equal(a.modes, b["modes"])
     np.testing.assert_array_equal(ta.total_movement_per_iter, b["movement"])
+
+
+@pytest.mark.parametrize("iters", [2, 40])
+def test_host_label_delivery_equals_device_labels(iters):
+    # host entry points on the sorted dense path copy cell0 during the loop
+    # and expand per-cell labels on the host threads (gs_engine.cu
+    # deliver_labels): identical to the device-written labels, also into an
+    # unaligned caller buffer and for runs too short to reach the run-ahead
+    # chunks (the copy is then issued after the loop)
+    import torch
+
+    x = W.cloud3d(2_500_001, seed=71)
+    cfg = gs.ShiftConfig(1.0, 1e-3, iters)
+    dev, k, it, mv, conv = gs.meanshiftpp_device(torch.from_numpy(x).cuda(), cfg)
+    dev = dev.cpu().numpy()
+    a, ta = gs.meanshiftpp_points(x, cfg)
+    assert np.array_equal(a.labels, dev) and a.k == k and ta.iterations == it
+    big = np.full(len(x) + 3, -7, dtype=np.int64)
+    out = big[3:]                       # 24-byte offset: not 64-byte aligned
+    b, _ = gs.meanshiftpp_points(x, cfg, labels_out=out)
+    assert np.array_equal(out, dev) and np.all(big[:3] == -7)
+    import ctypes as C
+
+    from paper_2104_00303_b200 import _lib
+
+    hb, db = C.c_int64(0), C.c_int64(0)
+    _lib.check(_lib.load().gs_fetch_transfer_bytes(_lib.context(), _lib.ref(hb), _lib.ref(db)))
+    assert hb.value == x.nbytes
+    assert 4 * len(x) < db.value < 8 * len(x)     # cell index + per-cell labels + modes
+    c, _ = gs.meanshiftpp(gs.PointSet(x), cfg)
+    assert np.array_equal(c.labels, dev)
