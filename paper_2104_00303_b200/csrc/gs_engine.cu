@@ -385,7 +385,7 @@ template <int D, class Tab>
 void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_pts) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const double* y0 = static_cast<const double*>(c->y[0].p);
-  launch(c, K_HIST, [&] { k_hist<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
+  launch(c, K_HIST, [&] { k_hist<D, Tab, false, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
 }
 
 // The table chain (k_agg -> k_derive -> k_agg ...) never reads the points:

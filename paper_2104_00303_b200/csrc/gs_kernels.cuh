@@ -131,6 +131,20 @@ __device__ __forceinline__ u64 pack_key(const GridParams& g, const double* v, bo
   return inside ? key : kEmpty;
 }
 
+// pack_key from the per-axis cells (integer-valued doubles) already taken
+template <int D>
+__device__ __forceinline__ u64 pack_cells(const GridParams& g, const double* f, bool& inside) {
+  u64 key = 0;
+  inside = true;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const i64 c = (i64)f[j];
+    inside &= (c >= g.lo[j]) & (c <= g.hi[j]);
+    key += (u64)(c - g.base[j]) * g.stride[j];
+  }
+  return inside ? key : kEmpty;
+}
+
 __device__ __forceinline__ void add128(u64& hi, u64& lo, u64 ohi, u64 olo) {
   const u64 l = lo + olo;
   hi += ohi + (l < lo ? 1ull : 0ull);
@@ -466,7 +480,9 @@ __device__ __forceinline__ bool load_quad(const double* __restrict__ y, const Gr
 // of a user-given point set, table dumps; the loop derives later tables).
 // Warps take strided super-tiles of kSuper consecutive 128-point tiles, so
 // the grid streams through a narrow window of memory.
-template <int D, class Tab, bool CountOnly = false>
+// Fresh: the input points of a run (first table) -- identical points are not
+// expected, so the per-quad / per-tile bitwise-identity tests are skipped.
+template <int D, class Tab, bool CountOnly = false, bool Fresh = false>
 __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(const double* __restrict__ y, i64 n, GridParams g,
                                                    Tab tab, Ctrl* ctrl, int check_done) {
   if (check_done && *(volatile int*)&ctrl->done) return;
@@ -497,12 +513,54 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(
           asm volatile("prefetch.global.L2 [%0];" ::"l"(y + (i64)j * g.ld + i0 + GS_HIST_PF * TILE));
       }
       double v[P][D];
-      bool uni;
-      const bool tu = load_quad<D>(y, g, i0, n, v, uni);
-      u64 key[P];
+      bool uni = false, tu = false;
+      if constexpr (Fresh) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double2* src = reinterpret_cast<const double2*>(y + (i64)j * g.ld + i0);
+          const double2 a = __ldcs(src), b = __ldcs(src + 1);
+          v[0][j] = a.x; v[1][j] = a.y; v[2][j] = b.x; v[3][j] = b.y;
+        }
+      } else {
+        tu = load_quad<D>(y, g, i0, n, v, uni);
+      }
       bool valid[P];
 #pragma unroll
       for (int m = 0; m < P; ++m) valid[m] = i0 + m < n;
+      if (!tu) {
+        // key-uniform tile (all 128 points in one cell, the common case on a
+        // cell-sorted iterate): decided on the per-axis floors, the key is
+        // packed once; the points add lane-privately into the spread carry
+        double f0[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) f0[j] = cell_of_fast(v[0][j], g.h, g.inv_h);
+        bool ku = valid[P - 1];
+        if (!uni) {
+#pragma unroll
+          for (int m = 1; m < P; ++m)
+#pragma unroll
+            for (int j = 0; j < D; ++j) ku &= cell_of_fast(v[m][j], g.h, g.inv_h) == f0[j];
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) ku &= __shfl_sync(kFull, f0[j], 0) == f0[j];
+        bool inside = false;
+        const u64 k0 = pack_cells<D>(g, f0, inside);
+        if (__all_sync(kFull, ku) && inside) {   // inside is warp-uniform here
+          if (k0 != ckey) {
+            if (dist) cagg.warp_sum();
+            if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
+            ckey = k0;
+            cagg.zero();
+          } else if (!dist && lane) {
+            cagg.zero();   // lane 0 keeps the (uniform) carry
+          }
+          dist = true;
+#pragma unroll
+          for (int m = 0; m < P; ++m) cagg.add(item_of<D, CountOnly>(g, v[m], true));
+          continue;
+        }
+      }
+      u64 key[P];
       if (uni) {
         bool inside;
         key[0] = pack_key<D>(g, v[0], inside);
@@ -518,26 +576,6 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(
             key[m] = pack_key<D>(g, v[m], inside);
             if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
           }
-        }
-      }
-      if (!tu) {
-        bool ku = valid[P - 1] & (key[0] != kEmpty);
-#pragma unroll
-        for (int m = 1; m < P; ++m) ku &= key[m] == key[0];
-        ku &= __shfl_sync(kFull, key[0], 0) == key[0];
-        if (__all_sync(kFull, ku)) {
-          if (key[0] != ckey) {
-            if (dist) cagg.warp_sum();
-            if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
-            ckey = key[0];
-            cagg.zero();
-          } else if (!dist && lane) {
-            cagg.zero();   // lane 0 keeps the (uniform) carry
-          }
-          dist = true;
-#pragma unroll
-          for (int m = 0; m < P; ++m) cagg.add(item_of<D, CountOnly>(g, v[m], true));
-          continue;
         }
       }
       if (dist) { cagg.warp_sum(); dist = false; }
