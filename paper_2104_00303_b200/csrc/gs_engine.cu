@@ -382,10 +382,14 @@ struct SortInfo {
 
 // Histogram of y[0] into table 0 (clean), before the loop.
 template <int D, class Tab>
-void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_pts) {
+void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_pts, bool grouped = false) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const double* y0 = static_cast<const double*>(c->y[0].p);
-  launch(c, K_HIST, [&] { k_hist<D, Tab, false, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
+  // grouped: y0 is the spatial sort's output (each cell's points contiguous)
+  if (grouped)
+    launch(c, K_HIST, [&] { k_hist<D, Tab, false, true, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
+  else
+    launch(c, K_HIST, [&] { k_hist<D, Tab, false, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
 }
 
 // The table chain (k_agg -> k_derive -> k_agg ...) never reads the points:
@@ -857,7 +861,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
     std::swap(c->y[0], c->y[1]);
     // table 0 from the sorted iterate (runs are contiguous: cheap), then the
     // occupied-slot list of the runs
-    enqueue_first_hist<D>(c, p, tabs, n, nb_pts);
+    enqueue_first_hist<D>(c, p, tabs, n, nb_pts, true);
     launch(c, K_SORT, [&] {
       k_compact<D><<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(tabs[0].ent, p.slots, si.runs, &ctrl->nruns);
     });
@@ -946,9 +950,9 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   if (table0)
     ;
   else if (p.dense)
-    enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
+    enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts, sorted);
   else
-    enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts);
+    enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts, sorted);
   // collapsed mode: after iteration 0 the runs of the spatial
   // sort hold one position each; later iterations move runs, not points
   const bool collapsed = c->collapsed && sorted && max_iters > 1;

@@ -482,7 +482,10 @@ __device__ __forceinline__ bool load_quad(const double* __restrict__ y, const Gr
 // the grid streams through a narrow window of memory.
 // Fresh: the input points of a run (first table) -- identical points are not
 // expected, so the per-quad / per-tile bitwise-identity tests are skipped.
-template <int D, class Tab, bool CountOnly = false, bool Fresh = false>
+// Grouped: the points of each cell are contiguous (the output of the spatial
+// sort), so a tile is key-uniform iff its first and last points share a cell:
+// two keys per tile instead of one per point.
+template <int D, class Tab, bool CountOnly = false, bool Fresh = false, bool Grouped = false>
 __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(const double* __restrict__ y, i64 n, GridParams g,
                                                    Tab tab, Ctrl* ctrl, int check_done) {
   if (check_done && *(volatile int*)&ctrl->done) return;
@@ -527,7 +530,32 @@ __global__ void __launch_bounds__(kThreads, (D <= 3 ? GS_HIST_MINB : 2)) k_hist(
       bool valid[P];
 #pragma unroll
       for (int m = 0; m < P; ++m) valid[m] = i0 + m < n;
-      if (!tu) {
+      if (Grouped && !tu) {
+        u64 kend = kEmpty;
+        if (lane == 0 || lane == 31) {
+          double w[D];
+#pragma unroll
+          for (int j = 0; j < D; ++j) w[j] = lane == 0 ? v[0][j] : v[P - 1][j];
+          bool inside;
+          kend = pack_key<D>(g, w, inside);
+        }
+        const u64 k0 = __shfl_sync(kFull, kend, 0);
+        const bool full_tile = __shfl_sync(kFull, (int)valid[P - 1], 31);
+        if (full_tile && k0 != kEmpty && k0 == __shfl_sync(kFull, kend, 31)) {
+          if (k0 != ckey) {
+            if (dist) cagg.warp_sum();
+            if (lane == 0) flush_segment<D, Tab, CountOnly>(tab, ctrl, ckey, cagg);
+            ckey = k0;
+            cagg.zero();
+          } else if (!dist && lane) {
+            cagg.zero();   // lane 0 keeps the (uniform) carry
+          }
+          dist = true;
+#pragma unroll
+          for (int m = 0; m < P; ++m) cagg.add(item_of<D, CountOnly>(g, v[m], true));
+          continue;
+        }
+      } else if (!tu) {
         // key-uniform tile (all 128 points in one cell, the common case on a
         // cell-sorted iterate): decided on the per-axis floors, the key is
         // packed once; the points add lane-privately into the spread carry
