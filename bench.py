@@ -325,6 +325,17 @@ def our_arm(a):
         if k in kernels and prof[k][0] > 0:
             kernels[k]["achieved_gbs"] = bytes_per[k] * work[k] / (prof[k][0] / 1e3) / 1e9
     launches = int(sum(v[1] for v in prof.values()))
+    # the histogram kernel's own roofline (north_star: shift and histogram
+    # each against the HBM peak); one launch per step, on the input
+    roof_hist = None
+    if prof["hist"][1] and prof["hist"][0] > 0:
+        ach = bytes_per["hist"] * work["hist"] / (prof["hist"][0] / 1e3) / 1e9
+        tr, tsrc = ncu_traffic("k_hist")
+        roof_hist = {"kernel": "k_hist", "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": tr, "peak_source": peak_src,
+                     "alg_bytes_per_launch": bytes_per["hist"],
+                     "bytes_note": "k_hist: reads the sorted fp64 iterate once, 8*d*n B",
+                     "avg_launch_ms": prof["hist"][0] / work["hist"], "traffic_source": tsrc}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": max(3, a.warmup), "ms_per_step": ms / a.steps, "higher_is_better": True,
@@ -332,7 +343,7 @@ def our_arm(a):
             "data": "synthetic (seeded numpy, paper_2104_00303_b200/workloads.py); fp32 input upcast "
                     "on device like PointSet (grid.py:43)",
             "config": workload_config(n, world), "iterations_per_step": per_step_iters,
-            "roofline": roof, "kernels": kernels,
+            "roofline": roof, "roofline_hist": roof_hist, "kernels": kernels,
             "kernels_note": "CUDA-event spans per kind over the timed region; agg/derive run on a "
                             "low-priority side stream concurrently with the shifts (their spans include "
                             "waiting for SM slots); see profiles/launches_r01_summary.json for serialised "

@@ -7,7 +7,12 @@ import re
 import sys
 
 src, out = sys.argv[1], sys.argv[2]
-rows = [r for r in csv.reader(open(src)) if len(r) > 10]
+if src.endswith(".gz"):
+    import gzip
+    fh = gzip.open(src, "rt")
+else:
+    fh = open(src)
+rows = [r for r in csv.reader(fh) if len(r) > 10]
 hdr = rows[0]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 agg = {}
