@@ -852,7 +852,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_shift(const double* y, double* 
 // CTA of T threads walks tiles of 4*T points; one thread keeps kShiftStages tiles
 // in flight with 1-D bulk copies (cp.async.bulk, completion on an mbarrier),
 // so the read stream needs no registers and no per-thread latency hiding.
-constexpr int kShiftStages = 3;
+#ifndef GS_SHIFT_STAGES
+#define GS_SHIFT_STAGES 2
+#endif
+constexpr int kShiftStages = GS_SHIFT_STAGES;
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
