@@ -150,29 +150,88 @@ def run_oracle(x, iters):
     return x.shape[0] * r["iterations"], dt, r["iterations"]
 
 
+def host_cpu():
+    """Host CPU model and logical core count."""
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
+
+
+def reference_engine():
+    """The unmodified reference engine from the reference install
+    (baseline/_ref, scripts/install_reference.sh), else None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "gridshift" / "modeseek.py").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        import gridshift.modeseek as rms
+        from gridshift.grid import PointSet as RPointSet
+    except Exception:   # noqa: BLE001 -- a broken install falls back to the port
+        return None
+    if getattr(rms.ENGINES["meanshiftpp"], "__gridshift_b200__", False):
+        return None     # patched by install(): not the reference's code path
+    return rms, RPointSet
+
+
+def run_reference_engine(x, iters, eng):
+    """ENGINES["meanshiftpp"](PointSet, ShiftConfig) of the reference itself
+    (modeseek.py:125,288), timed around the engine call only (its bench.py:44-51)."""
+    rms, RPointSet = eng
+    h, eta, _ = cfg4()
+    pts = RPointSet(x)
+    t0 = time.perf_counter()
+    _, tr = rms.ENGINES["meanshiftpp"](pts, rms.ShiftConfig(h=h, eta=eta, max_iters=iters))
+    dt = time.perf_counter() - t0
+    return x.shape[0] * tr.iterations, dt, tr.iterations
+
+
 def reference_arm(a):
+    """The reference's own CPU implementation on this host (rank 0 only):
+    the unmodified gridshift engine from baseline/_ref when installed
+    ("kind": "reference"), else its pinned numpy restatement ("port").
+    Each step is one engine call on a bounded sample of the cfg4 workload
+    (first 1M rows of the real input, iteration-capped), stated in
+    `reference_sample`; the metric is a rate, so the sample is comparable."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     budget = max(5.0, 150.0 / max(1, a.steps + a.warmup))
-    x, iters, what = cpu_sample(a.n, budget)
+    x_full = W.cloud3d(a.n)
+    x, iters, what = cpu_sample(a.n, budget, x_full)
+    del x_full
+    eng = reference_engine()
+    run = (lambda: run_reference_engine(x, iters, eng)) if eng else (lambda: run_oracle(x, iters))
     for _ in range(a.warmup):
-        run_oracle(x, iters)
-    ups, secs = 0, 0.0
+        run()
+    ups, secs, it = 0, 0.0, 0
     for _ in range(a.steps):
-        u, dt, _ = run_oracle(x, iters)
+        u, dt, it = run()
         ups += u
         secs += dt
     v = ups / secs
-    sample = f"{what}, {iters} iterations per step (max_iter cap), h=1, tol=1e-3"
+    kind = "reference" if eng else "port"
+    impl = ("gridshift.modeseek.ENGINES['meanshiftpp'] from baseline/_ref (unmodified reference)"
+            if eng else "oracle/gridshift_oracle.py (numpy restatement, bitwise-pinned to the reference)")
+    sample = f"{what} (uniform random subsample), {it} iterations per step (max_iter cap), h=1, tol=1e-3"
+    cfg = workload_config(a.n, 1)
+    cfg["reference_sample"] = {"rows": int(x.shape[0]), "iterations_per_step": int(it),
+                               "of": f"the cfg4 input (n={a.n:,}); value is the sample's point-updates/s"}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded numpy, paper_2104_00303_b200/workloads.py)",
-            "config": workload_config(a.n, a.gpus),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
-                             "note": "numpy restatement of gridshift (oracle/), bitwise-pinned to the "
-                                     "reference's outputs; the reference path is single-threaded"},
+            "config": cfg,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+                             "implementation": impl, "host_cpu": host_cpu(),
+                             "note": "the reference path is single-threaded numpy (unique/bincount/"
+                                     "searchsorted do not thread): 1 core"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -320,6 +379,11 @@ def our_arm(a):
                                "unchanged coordinate pairs are not rewritten); the full rewrite would be "
                                f"16*d*n = {16 * d * n_local} B") if kern == "shift" else None,
                 "avg_launch_ms": prof[kern][0] / work[kern], "traffic_source": tsrc}
+        if kern == "shift":
+            # the same launch time against SURVEY 8(d)'s full-rewrite bytes
+            # (16*d*n per launch); > 1 is possible only because unchanged
+            # coordinate pairs are not stored
+            roof["frac_s8d"] = 16 * d * n_local / (roof["avg_launch_ms"] / 1e3) / 1e9 / peak
     kernels = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
     for k in ("hist", "shift"):
         if k in kernels and prof[k][0] > 0:
@@ -348,7 +412,20 @@ def our_arm(a):
                             "low-priority side stream concurrently with the shifts (their spans include "
                             "waiting for SM slots); see profiles/launches_r01_summary.json for serialised "
                             "per-kernel device time",
-            "gpu_launches": launches, "clocks": clk.summary()}
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "byte_model": {
+                "executed": "per run: 1 per-point histogram pass (k_hist, 8*d*n B) on the sorted input; "
+                            "per iteration: 1 per-point shift (8*d*n B read + the changed 16-B coordinate "
+                            "pairs stored) + the O(cells) table chain (aggregate -> derive: table t+1 is "
+                            "derived per cell from table t, so points are not re-binned)",
+                "hist_passes_per_run": 1,
+                "shift_stored_bytes_per_iter_mean": stored_per_launch,
+                "shift_full_rewrite_bytes_per_iter": 16 * d * n_local,
+                "s8d_bytes_per_step": per_step_iters * 24 * d * n_local,
+                "s8d_step_frac": (per_step_iters * 24 * d * n_local) / (ms / a.steps / 1e3) / 1e9 / peak,
+                "note": "SURVEY 8(d) counts 24*d*n B per iteration (re-bin + full rewrite); s8d_step_frac is "
+                        "that byte count over the measured step time against the peak, > 1 because the "
+                        "engine does less work than 8(d) assumes, with bit-identical results"}}
 
     if shard:
         line["config"]["parallelism"] = f"rows sharded over {world} GPU(s), NCCL"
@@ -363,10 +440,14 @@ def our_arm(a):
             line["e2e"] = e2e(x_host, cfg, n, min(a.steps, 3))
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         x, iters, what = cpu_sample(n, 12.0, x_host)
-        ups, secs, it = run_oracle(x, iters)
-        line["cpu_baseline"] = {"value": ups / secs, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{what} (uniform random subsample), {it} iterations, "
-                                          f"oracle/gridshift_oracle.py (numpy, single-threaded)"}
+        eng = reference_engine()
+        ups, secs, it = run_reference_engine(x, iters, eng) if eng else run_oracle(x, iters)
+        line["cpu_baseline"] = {"value": ups / secs, "unit": UNIT, "cores": 1,
+                                "kind": "reference" if eng else "port",
+                                "sample": f"{what} (uniform random subsample), {it} iterations, " +
+                                          ("the unmodified reference engine (baseline/_ref)" if eng else
+                                           "oracle/gridshift_oracle.py (numpy, single-threaded)"),
+                                "host_cpu": host_cpu()}
     if shard:
         dist.barrier()
         dist.destroy_process_group()

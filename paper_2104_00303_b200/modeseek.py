@@ -63,7 +63,7 @@ class Labeling:
             raise ValueError("labels must cover [0, k) densely")
 
     @classmethod
-    def _from_engine(cls, labels, k, modes):
+    def _from_engine(cls, labels, k, modes, d):
         """Engine results are dense in [0, k) by construction (first-appearance
         ranks of every component; checked by the GPU tests), so skip the O(n)
         host-side re-validation of user-built Labelings (2 passes over 800 MB
@@ -72,8 +72,8 @@ class Labeling:
         obj.labels = np.ascontiguousarray(labels, dtype=np.int64)
         obj.modes = np.ascontiguousarray(modes, dtype=np.float64)
         obj.k = int(k)
-        if obj.k < 1 or obj.modes.shape != (obj.k, obj.modes.shape[1] if obj.modes.ndim == 2 else 0):
-            raise RuntimeError("engine returned malformed modes")
+        if obj.k < 1 or obj.modes.shape != (obj.k, int(d)):
+            raise RuntimeError(f"engine returned malformed modes {obj.modes.shape}, expected ({obj.k}, {d})")
         return obj
 
 
@@ -101,10 +101,38 @@ def _fetch(ctx, k: int, d: int, iters: int):
 
 def _finish(ctx, labels, k, d, iters, mv, conv):
     modes, kk, fp = _fetch(ctx, k, d, iters)
-    lab = Labeling._from_engine(labels, k, modes)
+    lab = Labeling._from_engine(labels, k, modes, d)
     tr = ShiftTrace(iterations=iters, total_movement_per_iter=mv[:iters].copy(),
                     converged=bool(conv), cells_per_iter=kk, fingerprint_per_iter=fp)
     return lab, tr
+
+
+def host_labels(labels_out, n: int) -> np.ndarray:
+    """The (n,) int64 host label buffer the C ABI writes n entries into:
+    a fresh array, or the caller's after checking shape, dtype and layout
+    (the engine's streaming-store expansion trusts it)."""
+    if labels_out is None:
+        return np.empty(n, dtype=np.int64)
+    if (not isinstance(labels_out, np.ndarray) or labels_out.shape != (n,)
+            or labels_out.dtype != np.int64 or not labels_out.flags.c_contiguous
+            or not labels_out.flags.writeable):
+        raise ValueError(f"labels_out must be a writeable C-contiguous ({n},) int64 array")
+    return labels_out
+
+
+def device_labels(labels_out, n: int, x):
+    """The (n,) int64 CUDA label tensor for the device entry points:
+    allocated on x's device, or the caller's after checking numel, dtype,
+    contiguity and device."""
+    import torch
+
+    if labels_out is None:
+        return torch.empty(n, dtype=torch.int64, device=x.device)
+    if (not isinstance(labels_out, torch.Tensor) or labels_out.numel() != n
+            or labels_out.dtype != torch.int64 or not labels_out.is_contiguous()
+            or labels_out.device != x.device):
+        raise ValueError(f"labels_out must be a contiguous int64 tensor of {n} elements on {x.device}")
+    return labels_out
 
 
 def meanshiftpp(points: PointSet, cfg: ShiftConfig, labels_out: np.ndarray | None = None
@@ -120,9 +148,7 @@ def meanshiftpp(points: PointSet, cfg: ShiftConfig, labels_out: np.ndarray | Non
     y = points.data
     n, d = y.shape
     eta = cfg.resolve_eta(n)
-    labels = np.empty(n, dtype=np.int64) if labels_out is None else labels_out
-    if labels.shape != (n,) or labels.dtype != np.int64 or not labels.flags.c_contiguous:
-        raise ValueError("labels_out must be a C-contiguous (n,) int64 array")
+    labels = host_labels(labels_out, n)
     mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
     k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
     _lib.check(L.gs_meanshiftpp(ctx, _lib.ptr(y), n, d, float(cfg.h), eta, int(cfg.max_iters),
@@ -147,7 +173,7 @@ def meanshiftpp_points(x: np.ndarray, cfg: ShiftConfig, labels_out: np.ndarray |
     ctx = _lib.context()
     n, d = x.shape
     eta = cfg.resolve_eta(n)
-    labels = np.empty(n, dtype=np.int64) if labels_out is None else labels_out
+    labels = host_labels(labels_out, n)
     mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
     k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
     dt = _lib.GS_DTYPE_F32 if x.dtype == np.float32 else _lib.GS_DTYPE_F64
@@ -174,18 +200,19 @@ def meanshiftpp_device(x, cfg: ShiftConfig, labels_out=None, stream=None, collap
     dtype = {torch.float64: _lib.GS_DTYPE_F64, torch.float32: _lib.GS_DTYPE_F32}.get(x.dtype)
     if dtype is None:
         raise ValueError("device point data must be float64 or float32")
-    if labels_out is None:
-        labels_out = torch.empty(n, dtype=torch.int64, device=x.device)
+    labels_out = device_labels(labels_out, n, x)
     eta = cfg.resolve_eta(n)
     mv = np.zeros(int(cfg.max_iters), dtype=np.float64)
     k, it, conv = C.c_int64(0), C.c_int32(0), C.c_int32(0)
     s = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
     _lib.check(L.gs_ctx_set_option(ctx, _lib.GS_OPT_COLLAPSED, 1 if collapsed else 0))
-    _lib.check(L.gs_meanshiftpp_device(ctx, C.c_void_p(x.data_ptr()), dtype, n, d, float(cfg.h),
-                                       eta, int(cfg.max_iters), C.c_void_p(labels_out.data_ptr()),
-                                       _lib.ref(k), _lib.ref(it), _lib.ptr(mv), _lib.ref(conv),
-                                       C.c_void_p(s)))
-    _lib.check(L.gs_ctx_set_option(ctx, _lib.GS_OPT_COLLAPSED, 0))
+    try:
+        _lib.check(L.gs_meanshiftpp_device(ctx, C.c_void_p(x.data_ptr()), dtype, n, d, float(cfg.h),
+                                           eta, int(cfg.max_iters), C.c_void_p(labels_out.data_ptr()),
+                                           _lib.ref(k), _lib.ref(it), _lib.ptr(mv), _lib.ref(conv),
+                                           C.c_void_p(s)))
+    finally:
+        _lib.check(L.gs_ctx_set_option(ctx, _lib.GS_OPT_COLLAPSED, 0))
     return labels_out, int(k.value), int(it.value), mv[: it.value].copy(), bool(conv.value)
 
 
@@ -227,14 +254,21 @@ ENGINES = {"meanshiftpp": meanshiftpp}
 
 
 def install(gridshift_module=None) -> None:
-    """Register this engine in a reference `gridshift` installation:
-    ENGINES["meanshiftpp"] (modeseek.py:288) and the direct imports in
-    track.py:22 / bench.py:23 resolve to the CUDA engine.  The reference's
-    own PointSet/ShiftConfig objects are accepted (same fields)."""
+    """Register this engine in a reference `gridshift` installation.
+
+    Patched (the reference's drop-in surfaces):
+    ENGINES["meanshiftpp"] (modeseek.py:288, read by segment_image, bench
+    and the CLI) and the module attributes `meanshiftpp`, `meanshiftpp_step`
+    and `extract_clusters` of gridshift.modeseek (modeseek.py:114,125,275),
+    plus track.py's direct import of meanshiftpp (track.py:22).  Callers
+    that import these names AFTER install() (e.g. the reference's own test
+    modules) get the CUDA engine; results come back as the reference's own
+    Labeling / ShiftTrace / PointSet objects."""
     import importlib
 
     gs = gridshift_module or importlib.import_module("gridshift")
     ms = importlib.import_module(gs.__name__ + ".modeseek")
+    rgrid = importlib.import_module(gs.__name__ + ".grid")
 
     def engine(points, cfg):
         lab, tr = meanshiftpp(PointSet(points.data), ShiftConfig(cfg.h, cfg.eta, cfg.max_iters))
@@ -243,8 +277,19 @@ def install(gridshift_module=None) -> None:
                               total_movement_per_iter=tr.total_movement_per_iter,
                               converged=tr.converged))
 
+    def step(points, cfg):
+        moved, mv = meanshiftpp_step(PointSet(points.data), ShiftConfig(cfg.h, cfg.eta, cfg.max_iters))
+        return rgrid.PointSet(moved.data), mv
+
+    def extract(converged, h):
+        lab = extract_clusters(PointSet(converged.data), h)
+        return ms.Labeling(labels=lab.labels, k=lab.k, modes=lab.modes)
+
+    engine.__gridshift_b200__ = step.__gridshift_b200__ = extract.__gridshift_b200__ = True
     ms.ENGINES["meanshiftpp"] = engine
     ms.meanshiftpp = engine
+    ms.meanshiftpp_step = step
+    ms.extract_clusters = extract
     for sub in ("track", "segment", "bench", "cli"):
         try:
             mod = importlib.import_module(gs.__name__ + "." + sub)

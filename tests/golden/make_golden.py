@@ -230,6 +230,23 @@ def make_tracking(store):
     del cfg
 
 
+def make_cfg3_full(out_dir: Path):
+    """cfg3 at BASELINE size: 300 frames of 1280x720, 128x128 window on the
+    object, h=16, B updated every frame (track.py:191-205).  Frames are not
+    stored: the GPU test regenerates them from workloads.tracking_video."""
+    vid, cen, _ = W.tracking_video()
+    frames = [Image(v) for v in vid]
+    win = track.Window(cx=float(round(cen[0, 0])), cy=float(round(cen[0, 1])), w=128, h_px=128)
+    cfg = ShiftConfig(h=16.0)
+    obj = _object_id(frames[0], win, cfg)
+    t0 = time.time()
+    rows = track.track_sequence(frames, win, cfg, [obj], update_bins=True)
+    wall = time.time() - t0
+    np.savez_compressed(out_dir / "big_cfg3_full.npz", win=np.array([win.cx, win.cy, win.w, win.h_px]),
+                        h=16.0, selected=obj, wall_s=wall, frames_digest=digest(vid),
+                        **_track_rows(rows))
+
+
 def make_big(out_dir: Path, which):
     for name in which:
         t0 = time.time()
@@ -242,9 +259,19 @@ def make_big(out_dir: Path, which):
         elif name == "cfg2":
             y = image_to_features(Image(W.cfg2_image(0)), "rgbxy", scale=0.25).data
             c = W.CONFIGS["cfg2"]
+        elif name.startswith("cfg2_img"):
+            y = image_to_features(Image(W.cfg2_image(int(name[8:]))), "rgbxy", scale=0.25).data
+            c = W.CONFIGS["cfg2"]
         elif name == "cfg4_10m":
             y = W.cloud3d(10_000_000).astype(np.float64)
             c = W.CONFIGS["cfg4"]
+        elif name == "cfg4_100m":
+            y = W.cloud3d(100_000_000).astype(np.float64)
+            c = W.CONFIGS["cfg4"]
+        elif name == "cfg3_full":
+            make_cfg3_full(out_dir)
+            print(f"cfg3_full {time.time() - t0:.1f}s", flush=True)
+            continue
         else:
             raise SystemExit(f"unknown big case {name}")
         r = run_engine(y, c["h"], c["eta"], c["max_iters"])
@@ -253,10 +280,14 @@ def make_big(out_dir: Path, which):
         small = lab.max() < 65536
         fields = dict(r, labels_digest=digest(lab), modes_digest=digest(r["modes"]),
                       n=y.shape[0], d=y.shape[1], wall_s=wall)
-        if small and name != "cfg4_10m":
+        if small and not name.startswith("cfg4"):
             fields["labels_u16"] = lab.astype(np.uint16)
+        if name == "cfg4_100m":
+            fields["label_sizes"] = np.bincount(lab, minlength=int(r["k"]))
+        n_rows, d_cols = y.shape
+        del y
         np.savez_compressed(out_dir / f"big_{name}.npz", **{k: np.asarray(v) for k, v in fields.items()})
-        print(f"{name}: n={y.shape[0]} iters={int(r['iterations'])} k={int(r['k'])} {wall:.1f}s", flush=True)
+        print(f"{name}: n={n_rows} iters={int(r['iterations'])} k={int(r['k'])} {wall:.1f}s", flush=True)
 
 
 def main():

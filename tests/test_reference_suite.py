@@ -1,0 +1,56 @@
+"""The reference's OWN tests, run against the CUDA engine (SURVEY.md 8c:
+"run these exact test functions against the new engine by monkeypatching
+ENGINES / meanshiftpp").
+
+The reference install (scripts/install_reference.sh -> baseline/_ref, the
+unmodified package plus its pkg/tests and pkg/assets) travels to the GPU box
+with the repo snapshot; tests/ref_engine_plugin.py installs the engine into
+it (paper_2104_00303_b200.install) before the reference's test modules
+import their names, then pytest runs the selected reference tests unmodified:
+
+  * test_modeseek.py: step KATs and the step-vs-oracle property
+    (:92-136), loop semantics (:141-236), extraction KATs (:241-316);
+  * test_acceptance.py: criterion 1, 200 random step instances including
+    points parked on faces (:38-61), criterion 4, engine agreement (:107-115),
+    criterion 5 (segmentation), criterion 8 (tracking, :173-214);
+  * test_track.py: tracker behaviour through the patched
+    track.meanshiftpp (:59-182).
+"""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+REF_TESTS = ROOT / "baseline" / "_ref" / "tests"
+
+SELECT = {
+    "test_modeseek.py": None,
+    "test_acceptance.py": "criterion_1 or criterion_4 or criterion_5 or criterion_8",
+    "test_track.py": None,
+}
+
+
+@pytest.mark.parametrize("module", sorted(SELECT))
+def test_reference_suite_on_cuda_engine(module, tmp_path):
+    if not (REF_TESTS / module).exists():
+        pytest.skip("reference install with its tests not present (scripts/install_reference.sh)")
+    calls = tmp_path / "calls.json"
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "tests.ref_engine_plugin",
+           "-p", "no:cacheprovider", "--rootdir", str(REF_TESTS), "-c", os.devnull,
+           str(REF_TESTS / module)]
+    if SELECT[module]:
+        cmd += ["-k", SELECT[module]]
+    env = dict(os.environ, GS_REF_CALLS=str(calls), PYTHONPATH=str(ROOT))
+    r = subprocess.run(cmd, cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=1800)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    n = json.loads(calls.read_text())
+    # the CUDA engine answered (not the reference's numpy path)
+    assert sum(n.values()) > 0, n
