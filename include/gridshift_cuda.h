@@ -118,6 +118,15 @@ GS_API int gs_segment_image(gs_ctx* ctx, const uint8_t* pixels, int32_t height, 
  * movement are the same exact integers; results are bit-identical).  The
  * per-point iterate is then not materialised after iteration 0. */
 #define GS_OPT_COLLAPSED 1
+/* GS_OPT_SUMS: 0 (default) = the reference's summation order, bit for bit:
+ * per-cell coordinate sums sequential in point order from 0.0 (np.bincount,
+ * grid.py:186-187) and neighbourhood sums sequential in lexicographic offset
+ * order (grid.py:253-258); 1 = order-independent exact sums rounded once
+ * (the row-sharded multi-GPU runs always use these: their result does not
+ * depend on how points are split across ranks). */
+#define GS_OPT_SUMS 2
+#define GS_SUMS_REFERENCE 0
+#define GS_SUMS_EXACT 1
 GS_API int gs_ctx_set_option(gs_ctx* ctx, int32_t option, int64_t value);
 
 /* Modes (k, d) of the last run on this context (Labeling.modes). */
@@ -131,6 +140,21 @@ GS_API int gs_fetch_trace(gs_ctx* ctx, int64_t* k_per_iter, uint64_t* fp_per_ite
  * iterate is updated in place and bitwise-unchanged coordinate pairs are not
  * rewritten; reads are always 8*d bytes per point).  Roofline accounting. */
 GS_API int gs_fetch_shift_bytes(gs_ctx* ctx, uint64_t* bytes_per_iter, int32_t cap);
+
+/* Final iterate y_T of the last per-point gs_meanshiftpp* run, in ORIGINAL
+ * point order, (n, d) row-major fp64 into host memory (modeseek.py:136-141:
+ * the `y` the reference hands to _extract).  Test observability: with
+ * GS_SUMS_REFERENCE it equals the reference's iterate bit for bit.  Not
+ * available after a collapsed-mode run (the per-point iterate is not
+ * materialised) -> GS_EINVAL. */
+GS_API int gs_fetch_iterate(gs_ctx* ctx, double* y_out, int64_t n);
+
+/* Reference-order sums of the last run (observability): per table (row 0 =
+ * the first table, row t+1 = the table derived in iteration t) five
+ * counters: segments folded in index order, of those the long ones taking
+ * the global radix sort, their points, the longest segment, and the
+ * single-source cells whose closed form was recomputed (not cached). */
+GS_API int gs_fetch_refsum_stats(gs_ctx* ctx, uint32_t* out, int32_t rows);
 
 /* Host<->device bytes of the last host entry point call (gs_meanshiftpp,
  * gs_meanshiftpp_host, gs_segment_image): the input upload, and the label

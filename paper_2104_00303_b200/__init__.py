@@ -11,6 +11,7 @@ from .batch import segment_batch
 from .grid import (CellTables, PointSet, bin_point, bin_points, build_cell_tables,
                    neighbor_aggregate, neighbor_stats)
 from .modeseek import (ENGINES, Labeling, ShiftConfig, ShiftTrace, extract_clusters, install,
+                       set_sum_order, sum_order,
                        meanshiftpp, meanshiftpp_device, meanshiftpp_points, meanshiftpp_step)
 from .segment import Image, SegmentMap, image_to_features, segment_image, segment_pixels
 from .track import (BinSet, TrackState, Window, cluster_window, init_tracker, neighborhood,
@@ -20,7 +21,7 @@ __all__ = [
     "BinSet", "CellTables", "ENGINES", "Image", "Labeling", "PointSet", "SegmentMap",
     "ShiftConfig", "ShiftTrace", "TrackState", "Window", "bin_point", "bin_points",
     "build_cell_tables", "cluster_window", "extract_clusters", "image_to_features",
-    "init_tracker", "install", "meanshiftpp", "meanshiftpp_device", "meanshiftpp_points", "meanshiftpp_step",
+    "init_tracker", "install", "set_sum_order", "sum_order", "meanshiftpp", "meanshiftpp_device", "meanshiftpp_points", "meanshiftpp_step",
     "neighbor_aggregate", "neighbor_stats", "neighborhood", "segment_batch", "segment_image", "segment_pixels",
     "track_frame", "track_sequence",
 ]

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgridshift_cuda.so"
 SOURCES = ["gs_engine.cu"]
-HEADERS = ["gs_common.cuh", "gs_kernels.cuh", "gs_track.cuh"]
+HEADERS = ["gs_common.cuh", "gs_kernels.cuh", "gs_refsum.cuh", "gs_track.cuh"]
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",

@@ -20,6 +20,7 @@ LIB_PATH = Path(os.environ.get("GRIDSHIFT_LIB", Path(__file__).resolve().parent 
 GS_OK, GS_EINVAL, GS_ERUNTIME, GS_EUNSUPPORTED = 0, 1, 2, 3
 GS_DTYPE_F64, GS_DTYPE_F32 = 0, 1
 GS_OPT_COLLAPSED = 1
+GS_OPT_SUMS, GS_SUMS_REFERENCE, GS_SUMS_EXACT = 2, 0, 1
 
 _P = C.c_void_p
 _i32 = C.c_int32
@@ -42,6 +43,8 @@ SIGNATURES = {
     "gs_ctx_set_option": (C.c_int, [_P, _i32, _i64]),
     "gs_fetch_trace": (C.c_int, [_P, _P, _P, _i32]),
     "gs_fetch_shift_bytes": (C.c_int, [_P, _P, _i32]),
+    "gs_fetch_iterate": (C.c_int, [_P, _P, _i64]),
+    "gs_fetch_refsum_stats": (C.c_int, [_P, _P, _i32]),
     "gs_fetch_transfer_bytes": (C.c_int, [_P, _P, _P]),
     "gs_profile": (C.c_int, [_P, _i32, _P, _P, _i32]),
     "gs_profile_kind": (C.c_char_p, [_i32]),
@@ -99,13 +102,33 @@ def default_device() -> int:
     return int(os.environ.get("GRIDSHIFT_DEVICE", os.environ.get("LOCAL_RANK", "0")))
 
 
+class _Contexts(dict):
+    """This thread's engine contexts (device -> gs_ctx*).  Held in a
+    threading.local, so it is released when its thread exits: every context
+    (streams, events, pinned and device buffers) is destroyed then, and a
+    long-lived process whose callers come from short-lived worker threads
+    (cli.py:206-216 opens a ThreadPoolExecutor per call) does not leak."""
+
+    def __del__(self):
+        lib = _lib
+        if lib is None:
+            return
+        for ctx in self.values():
+            try:
+                lib.gs_ctx_destroy(ctx)
+            except Exception:   # noqa: BLE001 -- interpreter shutdown
+                pass
+        self.clear()
+
+
 def context(device: int | None = None) -> C.c_void_p:
     """Per-thread, per-device engine context (contexts serialise calls, so
-    concurrent callers each get their own, cli.py:206-216 style)."""
+    concurrent callers each get their own, cli.py:206-216 style); destroyed
+    when the thread exits (_Contexts)."""
     dev = default_device() if device is None else int(device)
     cache = getattr(_tls, "ctx", None)
     if cache is None:
-        cache = _tls.ctx = {}
+        cache = _tls.ctx = _Contexts()
     ctx = cache.get(dev)
     if ctx is None:
         out = _P()
@@ -124,7 +147,7 @@ def ref(x):
     return C.byref(x)
 
 
-N_KINDS = 12
+N_KINDS = 13
 
 
 def profile(mode: int, device: int | None = None):

@@ -49,7 +49,7 @@ struct GridParams {
   u64 mask;                // hash mask (cap - 1) or 0 for dense tables
   i64 ld;                  // SoA leading dimension of the iterate (n rounded up to 128)
   double inv_h;            // fl(1 / h), for cell_of_fast
-  int debug;               // experiment switches (0 in production)
+  int pad_;                // (unused; keeps the layout)
 };
 
 // Device-resident loop control.  One per context.

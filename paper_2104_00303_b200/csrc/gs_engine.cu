@@ -23,6 +23,7 @@
 
 #include "../../include/gridshift_cuda.h"
 #include "gs_kernels.cuh"
+#include "gs_refsum.cuh"
 #include "gs_track.cuh"
 
 using namespace gs;
@@ -54,9 +55,9 @@ struct Buf {
 };
 
 enum Kind { K_INIT = 0, K_HIST, K_AGG, K_SHIFT, K_CLEAR, K_COMP, K_LABELS, K_XPOSE, K_DUMP, K_TRACK,
-            K_SORT, K_DERIVE, K_NKINDS };
+            K_SORT, K_DERIVE, K_REFSUM, K_NKINDS };
 const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "shift", "clear", "components",
-                                          "labels", "transpose", "dump", "track", "sort", "derive"};
+                                          "labels", "transpose", "dump", "track", "sort", "derive", "refsum"};
 
 constexpr int64_t kSortMinPoints = 1 << 15;   // spatial sort pays off above this
 
@@ -73,6 +74,36 @@ struct Prof {
 };
 
 }  // namespace
+
+// Reference-order sums of the current run (gs_refsum.cuh): device pointers
+// into the context's buffers, sized by rs_alloc.
+struct RsRun {
+  bool on = false;
+  int64_t n = 0;
+  u32 nblk = 0;          // radix tiles over n points
+  int maxpasses = 0;     // radix passes that can be needed for the segment ids
+  u64 segcap = 0;        // max segments (occupied cells)
+  double* rs[2] = {nullptr, nullptr};   // per table buffer: slots x D reference-order sums
+  u32 *nsrc = nullptr, *mid = nullptr, *outslot = nullptr, *rc[2] = {nullptr, nullptr}, *runkey = nullptr,
+      *runval = nullptr, *k[2] = {nullptr, nullptr}, *v[2] = {nullptr, nullptr}, *cnt = nullptr,
+      *scan = nullptr, *sstart = nullptr, *send = nullptr;
+  double *wsum = nullptr, *wpre = nullptr;
+  u64* wdelta = nullptr;
+  RsCtl* ctl = nullptr;
+  const u32* cell0 = nullptr;   // per point: run (initial slot)
+  const u32* runs = nullptr;    // occupied runs
+  const u32* nruns = nullptr;   // (device)
+  u64 slots = 0;                // loop table slots
+  // gathered segments (sorted runs): lengths, run lists
+  u32 *seglen = nullptr, *segbeg = nullptr, *segcur = nullptr, *seglist = nullptr, *runseg = nullptr,
+      *segscan = nullptr;
+  const u32 *start = nullptr, *end = nullptr, *perm = nullptr;   // the spatial sort's runs
+  bool all_big = true;          // no spatial sort: every segment takes the global sort
+  u64* runkv = nullptr;         // per run: pass-0 key (low) and value (high)
+  void* tag[2] = {nullptr, nullptr};   // per table buffer: Rec<D> the slot's closed form came from
+  u32* stats = nullptr;         // per table: 5 counters (k_rs_stats)
+  int stats_rows = 0;
+};
 
 struct gs_ctx {
   int device = 0;
@@ -124,6 +155,16 @@ struct gs_ctx {
   int64_t cell0_n = 0;
   int64_t xfer_h2d = 0, xfer_d2h = 0;   // last host call (gs_fetch_transfer_bytes)
   size_t slotlab_bytes = 0;
+  // reference-order sums (gs_refsum.cuh): option + buffers
+  bool exact_sums = false;              // GS_OPT_SUMS
+  // the last per-point run's iterate (gs_fetch_iterate)
+  int64_t it_n = 0;
+  int it_d = 0;
+  bool it_sorted = false, it_valid = false;
+  Buf rsb[2], rs_nsrc, rs_mid, rs_out, rs_rc[2], rs_rkey, rs_rval, rs_k[2], rs_v[2], rs_cnt, rs_scan,
+      rs_start, rs_end, rs_wsum, rs_wpre, rs_wdelta, rs_ctl, rs_cell0, rs_runs, rs_seglen, rs_segbeg,
+      rs_segcur, rs_seglist, rs_runseg, rs_segscan, rs_runkv, rs_tag[2], rs_stats, rs_lowrun;
+  RsRun rsr;
 };
 
 namespace {
@@ -224,7 +265,6 @@ Plan make_plan(int64_t n, int d, double h, const InitStats& s) {
   g.h = h;
   g.d = d;
   g.inv_h = 1.0 / h;
-  if (const char* dbg = getenv("GRIDSHIFT_DEBUG")) g.debug = atoi(dbg);
   __int128 prod = 1;
   double span2 = 0.0;
   int64_t ext[GS_MAXD];
@@ -346,6 +386,7 @@ InitStats run_init(gs_ctx* c, const Input& in, int64_t n, double h, double* y0) 
   for (int j = 0; j < GS_MAXD; ++j) {
     hs.cmin[j] = LLONG_MAX;
     hs.cmax[j] = LLONG_MIN;
+    hs.lowbit[j] = 4096;
   }
   *c->h_stats = hs;
   GS_CUDA(cudaMemcpyAsync(dst, c->h_stats, sizeof hs, cudaMemcpyHostToDevice, c->st));
@@ -372,11 +413,252 @@ struct SortInfo {
   u32* runs = nullptr;      // occupied initial slots
   u32* runroot = nullptr;   // per initial slot: final component root (scratch)
   u32* end = nullptr;       // per initial slot: run end (the scatter cursors)
+  u32* perm = nullptr;      // sorted position -> original index (reference-order sums only)
   uint64_t slots0 = 0;      // table slots at sort time (the range of cell0)
   double* runpos = nullptr; // collapsed mode: per-run positions (SoA, ld = rld)
   u32* runcnt = nullptr;
   int64_t rld = 0;
 };
+
+// ------------------------------------------------- reference-order sums
+// (gs_refsum.cuh).  rs_alloc sizes the buffers of one run; rs_first builds
+// the first table's sums, rs_next those of table t+1 right after k_derive.
+
+RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 segcap, int max_iters = 1) {
+  RsRun& R = c->rsr;
+  R.on = true;
+  R.n = n;
+  R.slots = p.slots;
+  R.segcap = std::max<u64>(segcap, 1);
+  R.nblk = (u32)((n + kRsTile - 1) / kRsTile);
+  const u64 mx = R.segcap - 1;
+  R.maxpasses = mx < 256 ? 1 : mx < 65536 ? 2 : mx < (1ull << 24) ? 3 : 4;
+  for (int b = 0; b < 2; ++b) {
+    R.rs[b] = ensure<double>(c, c->rsb[b], (size_t)p.slots * d);
+    R.rc[b] = ensure<u32>(c, c->rs_rc[b], runs_cap);
+    R.k[b] = ensure<u32>(c, c->rs_k[b], (size_t)n);
+    R.v[b] = ensure<u32>(c, c->rs_v[b], (size_t)n);
+  }
+  R.nsrc = ensure<u32>(c, c->rs_nsrc, p.slots);
+  R.mid = ensure<u32>(c, c->rs_mid, p.slots);
+  R.outslot = ensure<u32>(c, c->rs_out, R.segcap);
+  R.sstart = ensure<u32>(c, c->rs_start, R.segcap);
+  R.send = ensure<u32>(c, c->rs_end, R.segcap);
+  R.runkey = ensure<u32>(c, c->rs_rkey, runs_cap);
+  R.runval = ensure<u32>(c, c->rs_rval, runs_cap);
+  R.cnt = ensure<u32>(c, c->rs_cnt, 256ull * R.nblk);
+  R.scan = ensure<u32>(c, c->rs_scan, (256ull * R.nblk + kScan32Chunk - 1) / kScan32Chunk + 1);
+  const size_t nw = (size_t)(n / kFoldWin) + 1;
+  R.wsum = ensure<double>(c, c->rs_wsum, nw * d);
+  R.wpre = ensure<double>(c, c->rs_wpre, nw * d);
+  R.wdelta = ensure<u64>(c, c->rs_wdelta, nw * d);
+  R.ctl = ensure<RsCtl>(c, c->rs_ctl, 1);
+  R.seglen = ensure<u32>(c, c->rs_seglen, R.segcap);
+  R.segbeg = ensure<u32>(c, c->rs_segbeg, R.segcap + 1);
+  R.segcur = ensure<u32>(c, c->rs_segcur, R.segcap);
+  R.seglist = ensure<u32>(c, c->rs_seglist, std::max<u64>(runs_cap, R.segcap));
+  R.runseg = ensure<u32>(c, c->rs_runseg, std::max<u64>(runs_cap, R.segcap));
+  R.segscan = ensure<u32>(c, c->rs_segscan, (R.segcap + 1 + kScan32Chunk - 1) / kScan32Chunk + 1);
+  R.start = R.end = R.perm = nullptr;
+  R.all_big = true;
+  R.runkv = ensure<u64>(c, c->rs_runkv, runs_cap);
+  for (int b = 0; b < 2; ++b) {
+    const size_t tb = (size_t)p.slots * (d + 1) * sizeof(u64);
+    R.tag[b] = ensure<u64>(c, c->rs_tag[b], tb / 8);
+    GS_CUDA(cudaMemsetAsync(R.tag[b], 0, tb, c->st));
+  }
+  R.stats_rows = max_iters + 1;
+  R.stats = ensure<u32>(c, c->rs_stats, 5ull * R.stats_rows);
+  GS_CUDA(cudaMemsetAsync(R.stats, 0, 20ull * R.stats_rows, c->st));
+  GS_CUDA(cudaMemsetAsync(R.nsrc, 0, sizeof(u32) * p.slots, c->st));
+  GS_CUDA(cudaMemsetAsync(R.mid, 0xff, sizeof(u32) * p.slots, c->st));
+  return R;
+}
+
+// Stable radix sort of the fold elements by segment id (passes beyond the
+// device-side need exit at once).
+template <class Src0>
+void rs_sort(gs_ctx* c, RsRun& R, const Src0& src0) {
+  const u32 nb = R.nblk;
+  const int64_t ncnt = 256ll * nb;
+  const int nsb = (int)((ncnt + kScan32Chunk - 1) / kScan32Chunk);
+  for (int pass = 0; pass < R.maxpasses; ++pass) {
+    u32* ok = R.k[pass & 1];
+    u32* ov = R.v[pass & 1];
+    auto go = [&](const auto& src) {
+      using S = std::decay_t<decltype(src)>;
+      launch(c, K_REFSUM, [&] { k_rs_count<S><<<nb, kRsThreads, 0, c->st>>>(src, R.ctl, pass, R.cnt, nb); });
+      launch(c, K_REFSUM, [&] { k_scan32_reduce<<<nsb, 256, 0, c->st>>>(R.cnt, ncnt, R.scan, R.ctl, pass); });
+      launch(c, K_REFSUM, [&] { k_scan32_top<<<1, 1024, 0, c->st>>>(R.scan, nsb, R.ctl, pass); });
+      launch(c, K_REFSUM, [&] { k_scan32_apply<<<nsb, 256, 0, c->st>>>(R.cnt, ncnt, R.scan, R.ctl, pass); });
+      launch(c, K_REFSUM, [&] { k_rs_scatter<S><<<nb, kRsThreads, 0, c->st>>>(src, R.ctl, pass, R.cnt, nb, ok, ov); });
+    };
+    if (pass == 0)
+      go(src0);
+    else
+      go(RsBufSrc{R.k[(pass - 1) & 1], R.v[(pass - 1) & 1], &R.ctl->nelem});
+  }
+}
+
+template <int D, class Val>
+void rs_fold(gs_ctx* c, RsRun& R, const Val& V, double* rs_out) {
+  const RsSorted so{R.k[0], R.v[0], R.k[1], R.v[1]};
+  const int nbp = blocks_for(c, R.n);
+  const int64_t nw = R.n / kFoldWin;
+  const int nbw = (int)std::max<int64_t>(1, std::min<int64_t>((nw * 32 + 255) / 256, (int64_t)c->sms * 8));
+  const int nbs = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)R.segcap * 32 + 255) / 256, (int64_t)c->sms * 8));
+  launch(c, K_REFSUM, [&] { k_rs_bounds<<<nbp, 256, 0, c->st>>>(so, R.ctl, R.sstart, R.send); });
+  launch(c, K_REFSUM, [&] { k_fold_win<D, Val><<<nbw, 256, 0, c->st>>>(so, R.ctl, R.sstart, R.send, V, R.wsum); });
+  launch(c, K_REFSUM, [&] { k_fold_pre<D, Val><<<nbs, 256, 0, c->st>>>(so, R.ctl, R.sstart, R.send, V, R.wsum, R.wpre); });
+  launch(c, K_REFSUM, [&] { k_fold_delta<D, Val><<<nbw, 256, 0, c->st>>>(so, R.ctl, V, R.wsum, R.wpre, R.wdelta); });
+  launch(c, K_REFSUM, [&] {
+    k_fold_small<D, Val><<<blocks_for(c, (int64_t)R.segcap * D), 256, 0, c->st>>>(so, R.ctl, R.sstart, R.send, V,
+                                                                                 R.outslot, rs_out);
+  });
+  const int nbb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)R.segcap * D * 32 + 255) / 256, (int64_t)c->sms * 8));
+  launch(c, K_REFSUM, [&] {
+    k_fold_big<D, Val><<<nbb, 256, 0, c->st>>>(so, R.ctl, R.sstart, R.send, V, R.wdelta, R.outslot, rs_out);
+  });
+}
+
+// First table (table buffer 0 built): reference-order sums of y_0.  `si`:
+// the spatial sort's runs (nullptr: unsorted, every occupied cell is a run);
+// `ys`: the iterate the runs index (sorted layout); V: the input values in
+// ORIGINAL point order (the order np.bincount adds them in).
+template <int D, class Tab>
+void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si, const double* ys,
+              const InVal<D>& V, const InitStats& st) {
+  RsRun& R = c->rsr;
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  GS_CUDA(cudaMemsetAsync(R.ctl, 0, sizeof(RsCtl), c->st));
+  if (si) {
+    R.cell0 = si->cell0;
+    R.runs = si->runs;
+    R.nruns = &ctrl->nruns;
+    R.start = si->start;
+    R.end = si->end;
+    R.perm = si->perm;
+    R.all_big = si->perm == nullptr;
+  } else {
+    u32* c0 = ensure<u32>(c, c->rs_cell0, (size_t)n);
+    launch(c, K_REFSUM, [&] { k_rs_cell0<D, Tab><<<blocks_for(c, n), kThreads, 0, c->st>>>(ys, n, p.g, tabs[0], c0); });
+    R.cell0 = c0;
+    if constexpr (Tab::kDense) {
+      u32* rl = ensure<u32>(c, c->rs_runs, p.list_cap);
+      GS_CUDA(cudaMemsetAsync(&ctrl->nruns, 0, sizeof(u32), c->st));
+      launch(c, K_REFSUM, [&] {
+        k_compact<D><<<blocks_for(c, (int64_t)p.slots), kThreads, 0, c->st>>>(tabs[0].ent, p.slots, rl, &ctrl->nruns);
+      });
+      R.runs = rl;
+      R.nruns = &ctrl->nruns;
+    } else {
+      R.runs = tabs[0].list;
+      R.nruns = &ctrl->k[0];
+    }
+  }
+  LowBits lb;
+  bool coarse_ok = true;   // the global lowest bit proves every run exact already?
+  for (int j = 0; j < GS_MAXD; ++j) lb.v[j] = st.lowbit[j];
+  for (int j = 0; j < D; ++j) {
+    // |total| < n * max|x|: every run exact if the input's lowest bit is at
+    // least ulp of that (and of the fixed-point quantum)
+    double amax;
+    memcpy(&amax, &st.absmax[j], sizeof amax);
+    int e = 0;
+    frexp(amax * (double)n * (1.0 + 0x1p-40) + 1e-300, &e);
+    coarse_ok &= lb.v[j] >= -p.g.qexp[j] && lb.v[j] >= (e - 1) - 52;
+  }
+  int* lowrun = nullptr;
+  if (si && !coarse_ok) {
+    // per-run lowest bits over the sorted iterate (one pass)
+    lowrun = reinterpret_cast<int*>(ensure<u32>(c, c->rs_lowrun, (size_t)p.slots * D));
+    GS_CUDA(cudaMemsetAsync(lowrun, 0x7f, sizeof(int) * p.slots * D, c->st));   // large positive
+    const int nbl = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4096 + 1) * 32 / 256 + 1, (int64_t)c->sms * 8));
+    launch(c, K_REFSUM, [&] { k_rs_lowbit<D, Tab><<<nbl, 256, 0, c->st>>>(ys, n, p.g, tabs[0], lowrun); });
+  }
+  launch(c, K_REFSUM, [&] {
+    k_rs_first<D, Tab><<<blocks_for(c, (int64_t)p.list_cap), kThreads, 0, c->st>>>(
+        p.g, tabs[0], R.runs, R.nruns, si ? si->start : nullptr, ys, si != nullptr, !R.all_big, lb, R.rc[0],
+        R.runkey, R.outslot, R.rs[0], R.ctl, R.seglen, R.sstart, R.send, R.seglist, R.runkv, lowrun);
+  });
+  if (!R.all_big) {
+    launch(c, K_REFSUM, [&] {
+      k_rs_gather_warp<D, InVal<D>, true><<<c->sms * 8, 256, 0, c->st>>>(R.ctl, R.seglen, nullptr, R.seglist, R.start,
+                                                                         R.end, R.perm, nullptr, V, R.outslot,
+                                                                         R.rs[0], false);
+    });
+    static std::atomic<uint64_t> attr{0};
+    if (attr_pending(attr, c->device)) {
+      GS_CUDA(cudaFuncSetAttribute(k_rs_gather<D, InVal<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem));
+      attr_done(attr, c->device);
+    }
+    launch(c, K_REFSUM, [&] {
+      k_rs_gather<D, InVal<D>, true><<<c->sms * 2, 256, kGatherSmem, c->st>>>(R.ctl, R.seglen, nullptr, R.seglist, R.start,
+                                                                    R.end, R.perm, nullptr, V, R.outslot, R.rs[0],
+                                                                    false);
+    });
+  }
+  launch(c, K_REFSUM, [&] { k_rs_passes<<<1, 1, 0, c->st>>>(R.ctl); });
+  rs_sort(c, R, RsRunSrc{R.cell0, R.runkv, n});
+  rs_fold<D>(c, R, V, R.rs[0]);
+  launch(c, K_REFSUM, [&] { k_rs_stats<<<1, 1, 0, c->st>>>(R.ctl, R.stats); });
+  check_launch();
+}
+
+// Table t+1 (just derived into buffer (t+1)&1): its reference-order sums.
+template <int D, class Tab>
+void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
+  RsRun& R = c->rsr;
+  Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  const int cur = t & 1;
+  GS_CUDA(cudaMemsetAsync(R.ctl, 0, sizeof(RsCtl), c->st));
+  GS_CUDA(cudaMemsetAsync(R.segbeg, 0, sizeof(u32) * (R.segcap + 1), c->st));
+  GS_CUDA(cudaMemsetAsync(R.segcur, 0, sizeof(u32) * R.segcap, c->st));
+  const int64_t items = Tab::kDense ? (int64_t)p.slots : (int64_t)p.list_cap;
+  launch(c, K_REFSUM, [&] {
+    k_rs_classify<D, Tab><<<blocks_for(c, items), kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur, t,
+                                                                        R.nsrc, R.mid, R.outslot, R.rs[cur ^ 1], R.ctl,
+                                                                        R.seglen, R.sstart, R.send, R.all_big,
+                                                                        static_cast<Rec<D>*>(R.tag[cur ^ 1]));
+  });
+  const int nbr = blocks_for(c, (int64_t)p.list_cap);
+  launch(c, K_REFSUM, [&] {
+    k_rs_runs<D, Tab><<<nbr, kThreads, 0, c->st>>>(R.runs, R.nruns, R.rc[cur], R.rc[cur ^ 1], rec, tabs[cur ^ 1], R.mid,
+                                                   R.runkey, R.runval, ctrl, t, R.seglen, R.runseg, R.segbeg,
+                                                   R.all_big, R.runkv);
+  });
+  if (!R.all_big) {
+    // run lists of the gathered segments, then one CTA each
+    const int64_t ns = (int64_t)R.segcap + 1;
+    const int nsb = (int)((ns + kScan32Chunk - 1) / kScan32Chunk);
+    launch(c, K_REFSUM, [&] { k_scan32_reduce<<<nsb, 256, 0, c->st>>>(R.segbeg, ns, R.segscan, nullptr, 0); });
+    launch(c, K_REFSUM, [&] { k_scan32_top<<<1, 1024, 0, c->st>>>(R.segscan, nsb, nullptr, 0); });
+    launch(c, K_REFSUM, [&] { k_scan32_apply<<<nsb, 256, 0, c->st>>>(R.segbeg, ns, R.segscan, nullptr, 0); });
+    launch(c, K_REFSUM, [&] { k_rs_fill<<<nbr, kThreads, 0, c->st>>>(R.runs, R.nruns, R.runseg, R.segbeg, R.segcur, R.seglist); });
+    launch(c, K_REFSUM, [&] {
+      k_rs_gather_warp<D, RecVal<D>, false><<<c->sms * 8, 256, 0, c->st>>>(R.ctl, R.seglen, R.segbeg, R.seglist,
+                                                                          R.start, R.end, R.perm, R.runval,
+                                                                          RecVal<D>{rec}, R.outslot, R.rs[cur ^ 1],
+                                                                          false);
+    });
+    static std::atomic<uint64_t> attr{0};
+    if (attr_pending(attr, c->device)) {
+      GS_CUDA(cudaFuncSetAttribute(k_rs_gather<D, RecVal<D>, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem));
+      attr_done(attr, c->device);
+    }
+    launch(c, K_REFSUM, [&] {
+      k_rs_gather<D, RecVal<D>, false><<<c->sms * 2, 256, kGatherSmem, c->st>>>(R.ctl, R.seglen, R.segbeg, R.seglist, R.start,
+                                                                     R.end, R.perm, R.runval, RecVal<D>{rec},
+                                                                     R.outslot, R.rs[cur ^ 1], false);
+    });
+  }
+  launch(c, K_REFSUM, [&] { k_rs_passes<<<1, 1, 0, c->st>>>(R.ctl); });
+  rs_sort(c, R, RsRunSrc{R.cell0, R.runkv, R.n});
+  rs_fold<D>(c, R, RecVal<D>{rec}, R.rs[cur ^ 1]);
+  if (t + 1 < R.stats_rows) launch(c, K_REFSUM, [&] { k_rs_stats<<<1, 1, 0, c->st>>>(R.ctl, R.stats + 5 * (t + 1)); });
+  launch(c, K_REFSUM, [&] { k_rs_unmark<<<blocks_for(c, (int64_t)R.segcap), kThreads, 0, c->st>>>(R.outslot, R.ctl, R.mid); });
+  GS_CUDA(cudaMemsetAsync(R.nsrc, 0, sizeof(u32) * p.slots, c->st));
+}
 
 // -------------------------------------------------------------- iteration
 
@@ -556,6 +838,7 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     c->st = c->side;
   }
   bool bricked = false;
+  RsRun& R = c->rsr;
   if constexpr (D == 3 && Tab::kDense) {
     // dense 3-D lattice: tiled stencil over the occupied 8^3 bricks
     // (k_agg_brick3, k_derive_brick3); brick occupancy per table buffer
@@ -566,10 +849,12 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     const BrickMap bm{(u32)p.g.stride[0], (u32)p.g.stride[1], (u32)nby, (u32)nbz};
     static std::atomic<uint64_t> attr{0};
     if (attr_pending(attr, c->device)) {
-      GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBrickSmem));
-      // same (maximal) shared-memory carveout as k_shift_tma, so the chain's
-      // CTAs can be co-resident with the shift's on one SM
-      GS_CUDA(cudaFuncSetAttribute(k_agg_brick3, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      for (auto kern : {k_agg_brick3<true>, k_agg_brick3<false>}) {
+        GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBrickSmem));
+        // same (maximal) shared-memory carveout as k_shift_tma, so the chain's
+        // CTAs can be co-resident with the shift's on one SM
+        GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
       GS_CUDA(cudaFuncSetAttribute(k_derive_brick3, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       attr_done(attr, c->device);
     }
@@ -587,38 +872,45 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     u8* occ_cur = occ + (size_t)cur * nbr;
     u8* occ_nxt = occ + (size_t)(cur ^ 1) * nbr;
     launch(c, K_AGG, [&] {
-      k_agg_brick3<<<nbr, kBrickThreads, kBrickSmem, c->st>>>(
+      auto kern = R.on ? k_agg_brick3<true> : k_agg_brick3<false>;
+      kern<<<nbr, kBrickThreads, kBrickSmem, c->st>>>(
           p.g, tabs[cur], tabs[cur ^ 1], reinterpret_cast<Rec<3>*>(rec), ctrl,
           static_cast<u64*>(c->fp_hist.p) + t, static_cast<u32*>(c->k_hist.p) + t, nbx, nby, nbz, occ_cur, occ_nxt,
-          mask + (size_t)(cur ^ 1) * nbr * kMaskWords, mask + (size_t)cur * nbr * kMaskWords, t);
+          mask + (size_t)(cur ^ 1) * nbr * kMaskWords, mask + (size_t)cur * nbr * kMaskWords, t,
+          R.on ? R.rs[cur] : nullptr);
     });
     if (ov) GS_CUDA(cudaEventRecord(c->ev_rec[cur], c->st));
     launch(c, K_DERIVE, [&] {
       k_derive_brick3<<<nbr, kBrickThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1],
                                                         reinterpret_cast<const Rec<3>*>(rec), ctrl, nby, nbz, bm,
-                                                        occ_cur, occ_nxt, mask + (size_t)cur * nbr * kMaskWords, t);
+                                                        occ_cur, occ_nxt, mask + (size_t)cur * nbr * kMaskWords, t,
+                                                        R.on ? R.nsrc : nullptr);
     });
     bricked = true;
+    if (R.on) rs_next<D>(c, p, tabs, t, rec);
   }
+  const double* rs_cur = R.on ? R.rs[cur] : nullptr;
   if (!bricked && D >= 4 && !Tab::kDense)
     launch(c, K_AGG, [&] { k_agg_warp<D, Tab><<<c->sms * 8, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
                                                     ctrl, cur, static_cast<u64*>(c->fp_hist.p) + t,
-                                                    static_cast<u32*>(c->k_hist.p) + t, t); });
+                                                    static_cast<u32*>(c->k_hist.p) + t, t, rs_cur); });
   else if (!bricked)
     launch(c, K_AGG, [&] { k_agg<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur,
                                                     static_cast<u64*>(c->fp_hist.p) + t,
-                                                    static_cast<u32*>(c->k_hist.p) + t, t); });
+                                                    static_cast<u32*>(c->k_hist.p) + t, t, rs_cur); });
   if (!bricked && ov) GS_CUDA(cudaEventRecord(c->ev_rec[cur], c->st));
   if (!bricked)
     launch(c, K_DERIVE, [&] { k_derive<D, Tab><<<nb_cells, kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec,
-                                                                                  ctrl, cur, t); });
+                                                                                  ctrl, cur, t,
+                                                                                  R.on ? R.nsrc : nullptr); });
+  if (!bricked && R.on) rs_next<D>(c, p, tabs, t, rec);
   if (ov) {
     c->st = main_st;
     GS_CUDA(cudaStreamWaitEvent(main_st, c->ev_rec[cur], 0));
   }
   bool tma = false;
   if constexpr (Tab::kDense && D <= 3) {
-    // bulk-copy pipelined shift: persistent, 2 CTAs per SM
+    // bulk-copy pipelined shift: persistent, 8 CTAs of 64 threads per SM (2 TMA stages each)
     if (with_shift) {
       // 64-thread CTAs (tile = 256 points), 16 warps per SM: small CTAs
       // decouple the per-tile barriers (measured 256 -> 64: -1 ms per run)
@@ -821,6 +1113,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
   si.runs = ensure<u32>(c, c->runlist, p.list_cap);
   si.cell0 = ensure<u32>(c, c->cell0, (size_t)n);
   si.slots0 = p.slots;
+  si.perm = c->exact_sums ? nullptr : ensure<u32>(c, c->perm, (size_t)n);
   si.runroot = off;   // the cursors are dead once the scatter is done...
   si.end = off;       // ...except as run ends, read (collapsed mode) before runroot is written
   GS_CUDA(cudaMemsetAsync(si.minidx, 0xff, p.slots * sizeof(u32), c->st));
@@ -857,7 +1150,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
     launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, nullptr, nullptr, bsum, off, p.slots, si.start, off); });
     const int nchp = (int)((n + kRpt * kPlaceThreads - 1) / (kRpt * kPlaceThreads));
-    launch(c, K_SORT, [&] { k_bk_place<D, RT><<<nchp, kPlaceThreads, kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, y1, ctrl); });
+    launch(c, K_SORT, [&] { k_bk_place<D, RT><<<nchp, kPlaceThreads, kTallyWin * sizeof(u32), c->st>>>(stage, n, p.slots, p.g, off, y1, ctrl, si.perm); });
     std::swap(c->y[0], c->y[1]);
     // table 0 from the sorted iterate (runs are contiguous: cheap), then the
     // occupied-slot list of the runs
@@ -875,7 +1168,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
     launch(c, K_SORT, [&] { k_scan_top<<<1, 1024, 0, c->st>>>(bsum, nbs); });
     launch(c, K_SORT, [&] { k_scan_apply<D><<<nbs, kThreads, 0, c->st>>>(tabs[0].ent, list, &ctrl->k[0], bsum, off, p.slots, si.start); });
     double* stage = ensure<double>(c, c->stage, (size_t)n * StageRec<D>::W);
-    launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, stage, n, p.g, tabs[0], off, nullptr,
+    launch(c, K_SORT, [&] { k_scatter<D, Tab><<<nb_pts, kThreads, 0, c->st>>>(y0, stage, n, p.g, tabs[0], off, si.perm,
                                                                               si.cell0, si.minidx, ctrl); });
     launch(c, K_SORT, [&] { k_unstage<D><<<nb_pts, kThreads, 0, c->st>>>(stage, y1, n, p.g.ld); });
     clear_table<D>(c, p, tabs[0], &ctrl->k[0]);
@@ -953,6 +1246,21 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
     enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts, sorted);
   else
     enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts, sorted);
+  // reference-order sums (default): the first table's sums in np.bincount
+  // order, from the input values in original point order
+  if (!c->exact_sums) {
+    rs_alloc(c, p, D, n, sorted ? sinfo.slots0 : p.slots, p.list_cap, max_iters);
+    InVal<D> V{nullptr, 2, soa_ld(n)};
+    if (sorted && aos_in && p.dense)
+      V = InVal<D>{in.dev, in.kind == IN_F32 ? 1 : 0, 0};
+    else
+      V.p = sorted ? c->y[1].p : c->y[0].p;   // the fp64 iterate before the sort's swap
+    const double* ys = static_cast<const double*>(c->y[0].p);
+    if (p.dense)
+      rs_first<D>(c, p, tabs.dn, n, sorted ? &sinfo : nullptr, ys, V, s);
+    else
+      rs_first<D>(c, p, tabs.hs, n, sorted ? &sinfo : nullptr, ys, V, s);
+  }
   // collapsed mode: after iteration 0 the runs of the spatial
   // sort hold one position each; later iterations move runs, not points
   const bool collapsed = c->collapsed && sorted && max_iters > 1;
@@ -1053,6 +1361,11 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   GS_CUDA(cudaMemcpyAsync(c->iter_fp.data(), c->fp_hist.p, sizeof(u64) * r.iters, cudaMemcpyDeviceToHost, c->st));
   sync(c);
   for (int i = 0; i < r.iters; ++i) c->iter_k[i] = kk[i];
+  c->rsr.on = false;
+  c->it_n = n;
+  c->it_d = D;
+  c->it_sorted = sorted;
+  c->it_valid = !collapsed;
   return r;
 }
 
@@ -1095,13 +1408,19 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   GS_CUDA(cudaMemsetAsync(ensure<u32>(c, c->k_hist, 1), 0, 4, c->st));
   reset_ctrl(c);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
+  // reference-order sums: the step equals the reference's bit for bit
+  const bool rs = !c->exact_sums;
+  if (rs) rs_alloc(c, p, D, n, p.slots, p.list_cap);
+  const InVal<D> V{y0, 2, soa_ld(n)};
   if (p.dense) {
     enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts);
+    if (rs) rs_first<D>(c, p, tabs.dn, n, nullptr, y0, V, s);
     enqueue_iteration<D>(c, p, tabs.dn, 0, -1.0, n, nb_pts, nb_cells);
     clear_table<D>(c, p, tabs.dn[0], &ctrl->k[0]);
     clear_table<D>(c, p, tabs.dn[1], &ctrl->k[1]);
   } else {
     enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts);
+    if (rs) rs_first<D>(c, p, tabs.hs, n, nullptr, y0, V, s);
     enqueue_iteration<D>(c, p, tabs.hs, 0, -1.0, n, nb_pts, nb_cells);
     clear_table<D>(c, p, tabs.hs[0], &ctrl->k[0]);
     clear_table<D>(c, p, tabs.hs[1], &ctrl->k[1]);
@@ -1133,7 +1452,8 @@ int64_t dump_tables(gs_ctx* c, const Plan& p, Tab* tabs, int64_t cap, int64_t* c
       dnc = ensure<i64>(c, c->ranks, k);
       dns = ensure<double>(c, c->aux, (size_t)k * D);
     }
-    launch(c, K_DUMP, [&] { k_dump<D, Tab><<<blocks_for(c, k), kThreads, 0, c->st>>>(p.g, tabs[0], &ctrl->k[0], dk, dc, ds, dnc, dns); });
+    const double* rs = c->rsr.on ? c->rsr.rs[0] : nullptr;
+    launch(c, K_DUMP, [&] { k_dump<D, Tab><<<blocks_for(c, k), kThreads, 0, c->st>>>(p.g, tabs[0], &ctrl->k[0], dk, dc, ds, dnc, dns, rs); });
     check_launch();
     std::vector<u64> hk(k);
     std::vector<i64> hc(k), hnc(nc_out ? k : 0);
@@ -1180,12 +1500,18 @@ int64_t run_tables_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t
   reset_ctrl(c);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
+  // reference-order sums (default): the reference's tables bit for bit
+  const bool rs = !c->exact_sums;
+  if (rs) rs_alloc(c, p, D, n, p.slots, p.list_cap);
+  const InVal<D> V{y0, 2, soa_ld(n)};
   if (p.dense) {
     launch(c, K_HIST, [&] { k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.dn[0], ctrl, 0); });
+    if (rs) rs_first<D>(c, p, tabs.dn, n, nullptr, y0, V, s);
     build_list<D>(c, p, tabs.dn[0]);
     return dump_tables<D>(c, p, tabs.dn, cap, cells, counts, sums, nc, ns);
   }
   launch(c, K_HIST, [&] { k_hist<D><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs.hs[0], ctrl, 0); });
+  if (rs) rs_first<D>(c, p, tabs.hs, n, nullptr, y0, V, s);
   return dump_tables<D>(c, p, tabs.hs, cap, cells, counts, sums, nc, ns);
 }
 
@@ -1216,6 +1542,7 @@ int guarded(gs_ctx* c, F&& f) {
   try {
     GS_CUDA(cudaSetDevice(c->device));
     c->st = c->own;
+    c->rsr.on = false;   // set by the entry points that use reference-order sums
     f();
     return GS_OK;
   } catch (const Fail& e) {
@@ -1385,6 +1712,14 @@ void gs_ctx_destroy(gs_ctx* c) {
                  &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot, &c->bocc, &c->bmask, &c->wr_hist};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
+  Buf* rbufs[] = {&c->rsb[0], &c->rsb[1], &c->rs_nsrc, &c->rs_mid, &c->rs_out, &c->rs_rc[0], &c->rs_rc[1],
+                  &c->rs_rkey, &c->rs_rval, &c->rs_k[0], &c->rs_k[1], &c->rs_v[0], &c->rs_v[1], &c->rs_cnt,
+                  &c->rs_scan, &c->rs_start, &c->rs_end, &c->rs_wsum, &c->rs_wpre, &c->rs_wdelta, &c->rs_ctl,
+                  &c->rs_cell0, &c->rs_runs, &c->rs_seglen, &c->rs_segbeg, &c->rs_segcur, &c->rs_seglist,
+                  &c->rs_runseg, &c->rs_segscan, &c->rs_runkv, &c->rs_tag[0], &c->rs_tag[1], &c->rs_stats,
+                  &c->rs_lowrun};
+  for (Buf* b : rbufs)
+    if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->h_stats) cudaFreeHost(c->h_stats);
   if (c->h_small) cudaFreeHost(c->h_small);
@@ -1501,8 +1836,10 @@ int gs_ctx_set_option(gs_ctx* c, int32_t option, int64_t value) {
   return guarded(c, [&] {
     if (option == GS_OPT_COLLAPSED)
       c->collapsed = value != 0;
+    else if (option == GS_OPT_SUMS && (value == GS_SUMS_REFERENCE || value == GS_SUMS_EXACT))
+      c->exact_sums = value == GS_SUMS_EXACT;
     else
-      fail(GS_EINVAL, "unknown option");
+      fail(GS_EINVAL, "unknown option or value");
   });
 }
 
@@ -1548,6 +1885,32 @@ int gs_fetch_trace(gs_ctx* c, int64_t* k_per_iter, uint64_t* fp_per_iter, int32_
       if (k_per_iter) k_per_iter[i] = c->iter_k[i];
       if (fp_per_iter) fp_per_iter[i] = c->iter_fp[i];
     }
+  });
+}
+
+int gs_fetch_refsum_stats(gs_ctx* c, uint32_t* out, int32_t rows) {
+  return guarded(c, [&] {
+    if (!c->rsr.stats || rows > c->rsr.stats_rows) fail(GS_EINVAL, "no reference-order statistics of that size");
+    GS_CUDA(cudaMemcpyAsync(out, c->rsr.stats, 20ull * rows, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  });
+}
+
+int gs_fetch_iterate(gs_ctx* c, double* y_out, int64_t n) {
+  return guarded(c, [&] {
+    if (!c->it_valid || n != c->it_n || !y_out)
+      fail(GS_EINVAL, "no per-point iterate of that size from the last run on this context");
+    const int d = c->it_d;
+    double* out = ensure<double>(c, c->x_stage, (size_t)n * d);
+    const double* y = static_cast<const double*>(c->y[0].p);
+    const u32* cell0 = c->it_sorted ? static_cast<const u32*>(c->cell0.p) : nullptr;
+    const u32* start = c->it_sorted ? static_cast<const u32*>(c->runstart.p) : nullptr;
+    launch(c, K_XPOSE, [&] {
+      k_iterate_out<<<blocks_for(c, n), kThreads, 0, c->st>>>(y, soa_ld(n), d, cell0, start, n, out);
+    });
+    check_launch();
+    GS_CUDA(cudaMemcpyAsync(y_out, out, sizeof(double) * n * d, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
   });
 }
 

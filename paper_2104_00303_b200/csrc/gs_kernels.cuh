@@ -161,7 +161,18 @@ struct InitStats {
   u64 absmax[GS_MAXD];   // bit pattern of max |x| (non-negative doubles order as ints)
   int flags;
   int pad;
+  int lowbit[GS_MAXD];   // min over non-zero values of the exponent of their lowest set bit
 };
+
+// exponent of the lowest set bit of |v| (every value is a multiple of 2^it);
+// 4096 for zero
+__device__ __forceinline__ int lowbit_exp(double v) {
+  const u64 b = (u64)__double_as_longlong(v) & ~(1ull << 63);
+  if (!b) return 4096;
+  const int be = (int)(b >> 52);
+  const u64 mant = be ? ((b & ((1ull << 52) - 1)) | (1ull << 52)) : b;
+  return (be ? be : 1) - 1075 + __ffsll((long long)mant) - 1;
+}
 
 // y == nullptr: statistics only (the sorted path reads x directly).  The
 // cell range is taken from the extreme coordinates: fl(v/h) and floor are
@@ -171,8 +182,9 @@ __global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, 
                                                        i64 n, i64 ld, double h, InitStats* st) {
   const double inv_h = 1.0 / h;
   double vmin[D], vmax[D];
+  int low[D];
 #pragma unroll
-  for (int j = 0; j < D; ++j) { vmin[j] = INFINITY; vmax[j] = -INFINITY; }
+  for (int j = 0; j < D; ++j) { vmin[j] = INFINITY; vmax[j] = -INFINITY; low[j] = 4096; }
   int flags = 0;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -183,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, 
       if (!isfinite(v)) { flags |= kErrNonFinite; continue; }
       vmin[j] = fmin(vmin[j], v);
       vmax[j] = fmax(vmax[j], v);
+      low[j] = min(low[j], lowbit_exp(v));
     }
   }
   i64 cmin[D], cmax[D];
@@ -210,12 +223,15 @@ __global__ void __launch_bounds__(kThreads) k_init_aos(const T* __restrict__ x, 
     }
   }
   for (int o = 16; o; o >>= 1) flags |= __shfl_xor_sync(kFull, flags, o);
+#pragma unroll
+  for (int j = 0; j < D; ++j) low[j] = __reduce_min_sync(kFull, low[j]);
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       atomicMin((long long*)&st->cmin[j], (long long)cmin[j]);
       atomicMax((long long*)&st->cmax[j], (long long)cmax[j]);
       atomicMax((unsigned long long*)&st->absmax[j], (unsigned long long)amax[j]);
+      atomicMin(&st->lowbit[j], low[j]);
     }
     if (flags) atomicOr(&st->flags, flags);
   }
@@ -228,8 +244,9 @@ __global__ void __launch_bounds__(kThreads) k_init_image(const unsigned char* __
                                                          InitStats* st) {
   i64 cmin[D], cmax[D];
   u64 amax[D];
+  int low[D];
 #pragma unroll
-  for (int j = 0; j < D; ++j) { cmin[j] = LLONG_MAX; cmax[j] = LLONG_MIN; amax[j] = 0; }
+  for (int j = 0; j < D; ++j) { cmin[j] = LLONG_MAX; cmax[j] = LLONG_MIN; amax[j] = 0; low[j] = 4096; }
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     double v[D];
@@ -249,8 +266,11 @@ __global__ void __launch_bounds__(kThreads) k_init_image(const unsigned char* __
       cmin[j] = min(cmin[j], ci);
       cmax[j] = max(cmax[j], ci);
       amax[j] = max(amax[j], (u64)__double_as_longlong(fabs(v[j])));
+      low[j] = min(low[j], lowbit_exp(v[j]));
     }
   }
+#pragma unroll
+  for (int j = 0; j < D; ++j) low[j] = __reduce_min_sync(kFull, low[j]);
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     for (int o = 16; o; o >>= 1) {
@@ -265,6 +285,7 @@ __global__ void __launch_bounds__(kThreads) k_init_image(const unsigned char* __
       atomicMin((long long*)&st->cmin[j], (long long)cmin[j]);
       atomicMax((long long*)&st->cmax[j], (long long)cmax[j]);
       atomicMax((unsigned long long*)&st->absmax[j], (unsigned long long)amax[j]);
+      atomicMin(&st->lowbit[j], low[j]);
     }
   }
 }
@@ -1066,10 +1087,14 @@ __global__ void k_import_minima(Tab tab, const u32* kp, const u32* par, u32* fir
 // reduction of the exact 128-bit sums.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Tab prev, Rec<D>* __restrict__ rec,
-                                                       Ctrl* ctrl, int cur, u64* fp_out, u32* k_out, int t) {
+                                                       Ctrl* ctrl, int cur, u64* fp_out, u32* k_out, int t,
+                                                       const double* __restrict__ rs = nullptr) {
   if (block_stopped_before(ctrl, t)) return;
   constexpr int M = (D == 1) ? 3 : (D == 2) ? 9 : (D == 3) ? 27 : (D == 4) ? 81 :
                     (D == 5) ? 243 : (D == 6) ? 729 : (D == 7) ? 2187 : 6561;
+  // reference order: the lanes fetch 32 neighbours at a time into shared
+  // memory, lanes j < D then add axis j sequentially in offset order
+  __shared__ double nb_s[kThreads / 32][32][D];
   const int lane = threadIdx.x & 31;
   const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -1096,7 +1121,10 @@ __global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Ta
     u64 sh[D], sl[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) { sh[j] = 0; sl[j] = 0; }
-    for (int o = lane; o < M; o += 32) {
+    double rsum = 0.0;   // lane j < D: axis j in reference order
+    const int wl = threadIdx.x >> 5;
+    for (int o0 = 0; o0 < M; o0 += 32) {
+      const int o = o0 + lane;
       int r = o;
       i64 delta = 0;
 #pragma unroll
@@ -1105,14 +1133,33 @@ __global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Ta
         r /= 3;
       }
       u32 ns;
-      if (tab.find(key + (u64)delta, ns)) {
+      const bool hit = o < M && tab.find(key + (u64)delta, ns);
+      if (hit) {
         const Entry<D>& e = tab.ent[ns];
         cnt += e.count;
+        if (rs) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const i128 v = (((i128)(i64)e.hi[j]) << 32) + (i128)e.lo[j];
-          add128(sh[j], sl[j], (u64)((u128)v >> 64), (u64)v);
+          for (int j = 0; j < D; ++j) nb_s[wl][lane][j] = rs[(i64)ns * D + j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const i128 v = (((i128)(i64)e.hi[j]) << 32) + (i128)e.lo[j];
+            add128(sh[j], sl[j], (u64)((u128)v >> 64), (u64)v);
+          }
         }
+      }
+      if (rs) {
+        const unsigned hm = __ballot_sync(kFull, hit);
+        __syncwarp();
+        if (lane < D) {
+          unsigned mm = hm;
+          while (mm) {
+            const int q = __ffs(mm) - 1;
+            mm &= mm - 1;
+            rsum = __dadd_rn(rsum, nb_s[wl][q][lane]);
+          }
+        }
+        __syncwarp();
       }
     }
     for (int off = 16; off; off >>= 1) {
@@ -1124,12 +1171,16 @@ __global__ void __launch_bounds__(kThreads) k_agg_warp(GridParams g, Tab tab, Ta
         add128(sh[j], sl[j], oh, ol);
       }
     }
+    double rsv[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) rsv[j] = __shfl_sync(kFull, rsum, j);
     if (lane == 0) {
       Rec<D> rr;
       const double c = (double)cnt;
 #pragma unroll
       for (int j = 0; j < D; ++j)
-        rr.t[j] = __ddiv_rn(i128_to_double((i128)((((u128)sh[j]) << 64) | (u128)sl[j]), -g.qexp[j]), c);
+        rr.t[j] = rs ? __ddiv_rn(rsv[j], c)
+                     : __ddiv_rn(i128_to_double((i128)((((u128)sh[j]) << 64) | (u128)sl[j]), -g.qexp[j]), c);
       bool inside;
       rr.key = pack_key<D>(g, rr.t, inside);
       if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
@@ -1194,11 +1245,12 @@ __global__ void __launch_bounds__(kThreads) k_mark_bricks(const Entry<3>* ent, u
     if (ent[s].count) occ[bm.of((u32)s)] = 1;
 }
 
+template <bool RS>
 __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, DenseTable<3> tab, DenseTable<3> prev,
                                                               Rec<3>* __restrict__ rec, Ctrl* ctrl, u64* fp_out,
                                                               u32* k_out, int nbx, int nby, int nbz,
                                                               const u8* occ_cur, u8* occ_prev, const u32* pmask,
-                                                              u32* cmask, int t) {
+                                                              u32* cmask, int t, const double* __restrict__ rs) {
   if (block_stopped_before(ctrl, t)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   u64* E = reinterpret_cast<u64*>(smem_raw);          // [7][kH3] halo, then [7][kS2] y-pass
@@ -1227,7 +1279,20 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
     if (!cur_occ || q >= kH3) continue;
     const int hz = q % kHZ, hy = (q / kHZ) % kHY, hx = q / (kHZ * kHY);
     const int x = x0 + hx - 1, yv = y0 + hy - 1, z = z0 + hz - 1;
-    if (x >= 0 && yv >= 0 && z >= 0 && x < ext0 && yv < ext1 && z < ext2) v[u] = tab.ent[x * s0 + yv * s1 + z];
+    if (x >= 0 && yv >= 0 && z >= 0 && x < ext0 && yv < ext1 && z < ext2) {
+      const i64 sl = x * s0 + yv * s1 + z;
+      if constexpr (RS) {
+        // reference order: stage the count and the fp64 reference-order
+        // sums (bit patterns in the hi words; the lo words stay unused)
+        v[u].count = tab.ent[sl].count;
+        if (v[u].count) {
+#pragma unroll
+          for (int j = 0; j < 3; ++j) v[u].hi[j] = __double_as_longlong(rs[sl * 3 + j]);
+        }
+      } else {
+        v[u] = tab.ent[sl];
+      }
+    }
   }
   // clear the previous table in this brick (its cells are no longer read):
   // the occupancy bitmask its own k_agg_brick3 left (pmask) names the
@@ -1279,7 +1344,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
   // sparse brick (few occupied cells, typical once clusters contract): each
   // occupied cell gathers its 27 neighbours from the staged halo directly;
   // dense brick: separable z, y, x passes over the whole brick
-  const bool sparse = nocc <= kSparseCells;
+  const bool sparse = RS || nocc <= kSparseCells;
   if (!sparse) {
     // z-pass: S1[hx][hy][z] = E[hx][hy][z] + E[hx][hy][z+1] + E[hx][hy][z+2]
     for (int q = tid; q < kS1; q += blockDim.x) {
@@ -1308,6 +1373,36 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
     if (mine == 0) continue;
     const int lz = q % kBZ, ly = (q / kBZ) % kBY, lx = q / (kBZ * kBY);
     u64 wsum[kWords3];
+    if constexpr (RS) {
+      // 27 neighbours in lexicographic offset order (dx, dy, dz; grid.py:
+      // 199-208), each present one added in fp64 (grid.py:253-258)
+      u64 cn = 0;
+      double sm[3] = {0.0, 0.0, 0.0};
+      for (int dx = 0; dx < 3; ++dx)
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dz = 0; dz < 3; ++dz) {
+            const int h0 = ((lx + dx) * kHY + (ly + dy)) * kHZ + lz + dz;
+            const u64 cc = E[h0];
+            if (cc) {
+              cn += cc;
+#pragma unroll
+              for (int j = 0; j < 3; ++j) sm[j] = __dadd_rn(sm[j], __longlong_as_double((long long)E[(1 + j) * kH3 + h0]));
+            }
+          }
+      const u64 slot = (u64)(x0 + lx) * s0 + (u64)(y0 + ly) * s1 + (u64)(z0 + lz);
+      Rec<3> r;
+      const double c = (double)cn;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) r.t[j] = __ddiv_rn(sm[j], c);
+      bool inside;
+      r.key = pack_key<3>(g, r.t, inside);
+      if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
+      rec[slot] = r;
+      fp += cell_fingerprint<3>(g, slot, mine);
+      ++kc;
+      continue;
+    }
     if (sparse) {
 #pragma unroll
       for (int w = 0; w < kWords3; ++w) wsum[w] = 0;
@@ -1359,7 +1454,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_agg_brick3(GridParams g, Dens
 // target cell); the buffer receiving the new table was cleared by k_agg.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_derive(GridParams g, Tab cur, Tab nxt, const Rec<D>* __restrict__ rec,
-                                                     Ctrl* ctrl, int c, int t) {
+                                                     Ctrl* ctrl, int c, int t, u32* nsrc = nullptr) {
   if (block_stopped_before(ctrl, t)) return;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1378,6 +1473,8 @@ __global__ void __launch_bounds__(kThreads) k_derive(GridParams g, Tab cur, Tab 
       ag.lo[j] = (u64)(f & 0xffffffffll) * cnt;
     }
     flush_segment<D, Tab, false>(nxt, ctrl, r.key, ag);
+    // reference-order sums: how many source cells reach the target
+    if (nsrc) atomicAdd(nsrc + nxt.lookup(r.key), 1u);
   }
 }
 
@@ -1386,7 +1483,8 @@ __global__ void __launch_bounds__(kThreads) k_derive(GridParams g, Tab cur, Tab 
 __global__ void __launch_bounds__(kBrickThreads) k_derive_brick3(GridParams g, DenseTable<3> cur, DenseTable<3> nxt,
                                                                  const Rec<3>* __restrict__ rec, Ctrl* ctrl,
                                                                  int nby, int nbz, BrickMap bm, const u8* occ_cur,
-                                                                 u8* occ_nxt, const u32* cmask, int t) {
+                                                                 u8* occ_nxt, const u32* cmask, int t,
+                                                                 u32* nsrc) {
   if (block_stopped_before(ctrl, t)) return;
   if (!occ_cur[blockIdx.x]) return;
   // the brick's cell-occupancy mask (written by k_agg_brick3 for this table)
@@ -1443,6 +1541,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_derive_brick3(GridParams g, D
   }
   if (key == kEmpty || lane != __ffs(peers) - 1) return;
   flush_segment<3, DenseTable<3>, false>(nxt, ctrl, key, ag);
+  if (nsrc) atomicAdd(nsrc + key, (u32)__popc(peers));   // source cells reaching the target
   if (key < g.nkeys) occ_nxt[bm.of((u32)key)] = 1;
 }
 
@@ -1505,17 +1604,55 @@ __device__ __forceinline__ void neighbourhood_sum(const GridParams& g, const Tab
   }
 }
 
+// ------------------------------------------------------- neighbourhood sums
+// grid.py:253-258: hits in lexicographic offset order, each added in fp64
+// to an accumulator starting at 0.0; counts exact.
+
+template <int D, class Tab>
+__device__ __forceinline__ void neighbourhood_sum_rs(const GridParams& g, const Tab& tab, const double* __restrict__ rs,
+                                                     u64 key, u64& cnt, double* sum) {
+  constexpr int M = (D == 1) ? 3 : (D == 2) ? 9 : (D == 3) ? 27 : (D == 4) ? 81 :
+                    (D == 5) ? 243 : (D == 6) ? 729 : (D == 7) ? 2187 : 6561;
+  cnt = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) sum[j] = 0.0;
+  for (int o = 0; o < M; ++o) {
+    int r = o;
+    i64 delta = 0;
+#pragma unroll
+    for (int j = D - 1; j >= 0; --j) {
+      delta += (i64)((r % 3) - 1) * (i64)g.stride[j];
+      r /= 3;
+    }
+    u32 ns;
+    if (tab.find(key + (u64)delta, ns)) {
+      cnt += tab.ent[ns].count;
+#pragma unroll
+      for (int j = 0; j < D; ++j) sum[j] = __dadd_rn(sum[j], rs[(i64)ns * D + j]);
+    }
+  }
+}
+
 template <int D, class Tab>
 __device__ __forceinline__ void agg_cell(const GridParams& g, const Tab& tab, u32 s, Rec<D>* __restrict__ rec,
-                                         u64& fp, Ctrl* ctrl) {
+                                         u64& fp, Ctrl* ctrl, const double* __restrict__ rs) {
   const u64 key = tab.key_of(s);
   u64 cnt;
-  i128 sum[D];
-  neighbourhood_sum<D>(g, tab, key, cnt, sum);
-  const double c = (double)cnt;
   Rec<D> r;
+  if (rs) {
+    // reference order (grid.py:253-258, modeseek.py:109)
+    double sum[D];
+    neighbourhood_sum_rs<D>(g, tab, rs, key, cnt, sum);
+    const double c = (double)cnt;
 #pragma unroll
-  for (int j = 0; j < D; ++j) r.t[j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
+    for (int j = 0; j < D; ++j) r.t[j] = __ddiv_rn(sum[j], c);
+  } else {
+    i128 sum[D];
+    neighbourhood_sum<D>(g, tab, key, cnt, sum);
+    const double c = (double)cnt;
+#pragma unroll
+    for (int j = 0; j < D; ++j) r.t[j] = __ddiv_rn(i128_to_double(sum[j], -g.qexp[j]), c);
+  }
   bool inside;
   r.key = pack_key<D>(g, r.t, inside);
   if (!inside) atomicOr(&ctrl->error, kErrOutOfBox);
@@ -1530,7 +1667,8 @@ __device__ __forceinline__ void agg_cell(const GridParams& g, const Tab& tab, u3
 // of this iteration; the last CTA resets the cleared table's cell count.
 template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab prev, Rec<D>* __restrict__ rec,
-                                                  Ctrl* ctrl, int cur, u64* fp_out, u32* k_out, int t) {
+                                                  Ctrl* ctrl, int cur, u64* fp_out, u32* k_out, int t,
+                                                  const double* __restrict__ rs = nullptr) {
   if (block_stopped_before(ctrl, t)) return;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1548,7 +1686,7 @@ __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab pre
     }
     for (i64 s = tid; s < ns; s += stride) {
       if (tab.ent[s].count == 0) continue;
-      agg_cell<D>(g, tab, (u32)s, rec, fp, ctrl);
+      agg_cell<D>(g, tab, (u32)s, rec, fp, ctrl, rs);
       ++kc;
     }
   } else {
@@ -1563,7 +1701,7 @@ __global__ void __launch_bounds__(kThreads) k_agg(GridParams g, Tab tab, Tab pre
     }
     const u32 k = ctrl->k[cur];
     for (i64 a = tid; a < k; a += stride) {
-      agg_cell<D>(g, tab, tab.list[a], rec, fp, ctrl);
+      agg_cell<D>(g, tab, tab.list[a], rec, fp, ctrl, rs);
       ++kc;
     }
   }
@@ -2209,7 +2347,7 @@ __global__ void __launch_bounds__(kTallyThreads) k_bk_tally(const uint4* __restr
 // local ranks, SoA fp64 writes of the sorted iterate (off ends as run ends)
 template <int D, typename RT>
 __global__ void __launch_bounds__(kPlaceThreads) k_bk_place(const uint4* __restrict__ stage, i64 n, u64 nslots, GridParams g,
-                                                  u32* off, double* __restrict__ ys, Ctrl* ctrl) {
+                                                  u32* off, double* __restrict__ ys, Ctrl* ctrl, u32* perm) {
   constexpr int WIN = kTallyWin;
   constexpr int V = SRec<D, RT>::kVec;
   extern __shared__ u32 cnt[];
@@ -2249,6 +2387,7 @@ __global__ void __launch_bounds__(kPlaceThreads) k_bk_place(const uint4* __restr
     srec_coords<D, RT>(stage + (r0 + t * kPlaceThreads + threadIdx.x) * V, v);
 #pragma unroll
     for (int j = 0; j < D; ++j) __stcs(ys + (i64)j * g.ld + pos[t], v[j]);
+    if (perm) perm[pos[t]] = idx[t];   // sorted position -> original index
   }
 }
 
@@ -2504,7 +2643,7 @@ __global__ void k_reset_count(u32* kp) { *kp = 0; }
 // Occupied-cell dump for build_cell_tables / neighbour stats (grid.py:193, 230).
 template <int D, class Tab>
 __global__ void k_dump(GridParams g, Tab tab, const u32* kp, u64* keys_out, i64* counts_out,
-                       double* sums_out, i64* ncounts_out, double* nsums_out) {
+                       double* sums_out, i64* ncounts_out, double* nsums_out, const double* rs = nullptr) {
   const u32 k = *kp;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 a = (i64)blockIdx.x * blockDim.x + threadIdx.x; a < k; a += stride) {
@@ -2516,15 +2655,22 @@ __global__ void k_dump(GridParams g, Tab tab, const u32* kp, u64* keys_out, i64*
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const i128 v = (((i128)(i64)e.hi[j]) << 32) + (i128)e.lo[j];
-      sums_out[a * D + j] = i128_to_double(v, -g.qexp[j]);
+      sums_out[a * D + j] = rs ? rs[(i64)s * D + j] : i128_to_double(v, -g.qexp[j]);
     }
     if (ncounts_out) {
       u64 cnt;
-      i128 sum[D];
-      neighbourhood_sum<D>(g, tab, key, cnt, sum);
-      ncounts_out[a] = (i64)cnt;
+      if (rs) {
+        double sum[D];
+        neighbourhood_sum_rs<D>(g, tab, rs, key, cnt, sum);
 #pragma unroll
-      for (int j = 0; j < D; ++j) nsums_out[a * D + j] = i128_to_double(sum[j], -g.qexp[j]);
+        for (int j = 0; j < D; ++j) nsums_out[a * D + j] = sum[j];
+      } else {
+        i128 sum[D];
+        neighbourhood_sum<D>(g, tab, key, cnt, sum);
+#pragma unroll
+        for (int j = 0; j < D; ++j) nsums_out[a * D + j] = i128_to_double(sum[j], -g.qexp[j]);
+      }
+      ncounts_out[a] = (i64)cnt;
     }
   }
 }

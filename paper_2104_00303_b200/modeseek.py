@@ -135,6 +135,37 @@ def device_labels(labels_out, n: int, x):
     return labels_out
 
 
+SUM_ORDERS = {"reference": _lib.GS_SUMS_REFERENCE, "exact": _lib.GS_SUMS_EXACT}
+
+
+def set_sum_order(order: str, device: int | None = None) -> None:
+    """Summation order of this thread's engine context.
+
+    "reference" (default): every per-cell coordinate sum is the reference's
+    sequential fp64 sum in point order (np.bincount, grid.py:186-187) and
+    every neighbourhood sum its sequential sum in lexicographic offset order
+    (grid.py:253-258) -- iterates equal the reference's bit for bit.
+    "exact": order-independent exact fixed-point sums rounded once (what the
+    row-sharded multi-GPU path computes, independent of the split)."""
+    if order not in SUM_ORDERS:
+        raise ValueError(f"sum order must be one of {sorted(SUM_ORDERS)}, got {order!r}")
+    _lib.check(_lib.load().gs_ctx_set_option(_lib.context(device), _lib.GS_OPT_SUMS, SUM_ORDERS[order]))
+
+
+class sum_order:
+    """Context manager: `with sum_order("exact"): ...` (this thread)."""
+
+    def __init__(self, order: str, device: int | None = None):
+        self.order, self.device = order, device
+
+    def __enter__(self):
+        set_sum_order(self.order, self.device)
+        return self
+
+    def __exit__(self, *exc):
+        set_sum_order("reference", self.device)
+
+
 def meanshiftpp(points: PointSet, cfg: ShiftConfig, labels_out: np.ndarray | None = None
                 ) -> tuple[Labeling, ShiftTrace]:
     """modeseek.py:125-146 on the B200: device-resident loop until the
@@ -214,6 +245,25 @@ def meanshiftpp_device(x, cfg: ShiftConfig, labels_out=None, stream=None, collap
     finally:
         _lib.check(L.gs_ctx_set_option(ctx, _lib.GS_OPT_COLLAPSED, 0))
     return labels_out, int(k.value), int(it.value), mv[: it.value].copy(), bool(conv.value)
+
+
+def last_iterate(n: int, d: int, device: int | None = None) -> np.ndarray:
+    """Final iterate (n, d) of this thread's last per-point run, original
+    point order (test observability: the trajectory check against the
+    reference/oracle bit for bit)."""
+    y = np.empty((n, d), dtype=np.float64)
+    _lib.check(_lib.load().gs_fetch_iterate(_lib.context(device), _lib.ptr(y), n))
+    return y
+
+
+def last_refsum_stats(iterations: int, device: int | None = None) -> np.ndarray:
+    """Reference-order sum counters of this thread's last run, one row per
+    table (row 0 = first table): segments folded in index order, long
+    segments taking the global sort, their points, longest segment,
+    recomputed single-source closed forms."""
+    out = np.zeros((iterations + 1, 5), dtype=np.uint32)
+    _lib.check(_lib.load().gs_fetch_refsum_stats(_lib.context(device), _lib.ptr(out), iterations + 1))
+    return out
 
 
 def last_modes(k: int, d: int, device: int | None = None) -> np.ndarray:

@@ -37,3 +37,13 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture
+def exact_sums():
+    """Run the engine with order-independent exact sums (GS_SUMS_EXACT) --
+    the tests that pin every device reduction against tests/exact_model.py."""
+    import paper_2104_00303_b200 as gs
+
+    with gs.sum_order("exact"):
+        yield

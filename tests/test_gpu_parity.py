@@ -40,8 +40,12 @@ def test_tables_vs_reference(c):
     assert np.array_equal(t.nbr_counts, f["nbr_counts"])
     scale = np.abs(f["y"]).max()
     np.testing.assert_allclose(t.nbr_sums, f["nbr_sums"], rtol=1e-12, atol=1e-15 * scale * len(f["y"]))
+    # reference-order sums (the default): np.bincount's sums bit for bit
+    assert np.array_equal(t.sums, f["sums"])
+    assert np.array_equal(t.nbr_sums, f["nbr_sums"])
 
 
+@pytest.mark.usefixtures("exact_sums")
 def test_tables_exact_sums():
     # exact device sums == math.fsum of the member coordinates
     rng = np.random.default_rng(5)
@@ -63,6 +67,8 @@ def test_step_vs_reference(c):
     f = G.case("steps", c)
     moved, mv = gs.meanshiftpp_step(gs.PointSet(f["y"]), gs.ShiftConfig(h=float(f["h"])))
     want = f["y_next"]
+    # reference-order sums (the default): the reference's step bit for bit
+    assert np.array_equal(moved.data, want)
     rel = np.abs(moved.data - want).max() / max(np.abs(want).max(), 1e-30)
     assert rel <= 1e-10
     assert mv == pytest.approx(float(f["movement"]), rel=1e-9, abs=1e-12)
@@ -78,6 +84,7 @@ def _exact_step(y, h):
     return out
 
 
+@pytest.mark.usefixtures("exact_sums")
 @pytest.mark.parametrize("d", [1, 2, 3, 4, 5])
 def test_step_is_exactly_rounded(d):
     # values in [1, 2): fixed-point capture is exact, so the device result is
@@ -137,6 +144,38 @@ def test_run_vs_reference(c):
     _check_run(lab, tr, f, h)
 
 
+@pytest.mark.parametrize("c", G.cases("runs"))
+def test_run_trajectory_bitwise_vs_reference(c):
+    """Reference-order sums (the default): the final iterate -- hence every
+    iterate -- equals the reference's bit for bit (the oracle reproduces the
+    reference bitwise on these fixtures, test_oracle.py), the iteration
+    count and labels are the reference's, and the modes differ only by the
+    reference's own rounding of the mode means (exact here, sequential
+    there: modeseek.py:268-271)."""
+    f = G.case("runs", c)
+    h = float(f["h"])
+    y0 = f["y"]
+    lab, tr = gs.meanshiftpp(gs.PointSet(y0), gs.ShiftConfig(h=h, eta=_eta(f), max_iters=int(f["max_iters"])))
+    r = O.meanshiftpp(y0, h, _eta(f), int(f["max_iters"]))
+    assert tr.iterations == r["iterations"] == int(f["iterations"])
+    assert tr.converged == r["converged"]
+    y = gs.modeseek.last_iterate(*y0.shape)
+    assert np.array_equal(y, r["y"])
+    assert np.array_equal(lab.labels, f["labels"])
+    np.testing.assert_allclose(lab.modes, f["modes"], rtol=1e-13, atol=1e-13 * h)
+
+
+def test_cfg0_trajectory_bitwise_vs_reference():
+    c = W.CONFIGS["cfg0"]
+    y0 = W.blobs2d()
+    lab, tr = gs.meanshiftpp(gs.PointSet(y0), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]))
+    r = O.meanshiftpp(y0, c["h"], c["eta"], c["max_iters"])
+    assert tr.iterations == r["iterations"]
+    assert np.array_equal(gs.modeseek.last_iterate(*y0.shape), r["y"])
+    assert np.array_equal(lab.labels, r["labels"])
+
+
+@pytest.mark.usefixtures("exact_sums")
 @pytest.mark.parametrize("c", G.cases("runs"))
 def test_run_bitwise_vs_exact_model(c):
     # every device reduction pinned: the GPU equals the exact-arithmetic
@@ -322,8 +361,21 @@ def test_cfg4_10m_vs_reference():
     assert tr.iterations == int(f["iterations"])
     assert [int(v) for v in tr.fingerprint_per_iter] == [int(v) for v in f["iter_fp"]]
     assert _digest(lab.labels) == str(f["labels_digest"])
-    _check_model(lab, tr, f, h)
     _modes_vs_reference(lab, f, h, "cfg4@10M")
+
+
+@pytest.mark.slow
+@pytest.mark.usefixtures("exact_sums")
+def test_cfg4_10m_exact_model_bitwise():
+    """GS_SUMS_EXACT: bit for bit the exact-arithmetic model (every device
+    reduction pinned); the reference's sequential sums sit 1.73e-9*h away
+    from exact arithmetic after 50 creeping iterations."""
+    f = G.big("cfg4_10m")
+    c = W.CONFIGS["cfg4"]
+    y = W.cloud3d(10_000_000).astype(np.float64)
+    lab, tr = gs.meanshiftpp(gs.PointSet(y), gs.ShiftConfig(c["h"], c["eta"], c["max_iters"]))
+    assert [int(v) for v in tr.fingerprint_per_iter] == [int(v) for v in f["iter_fp"]]
+    _check_model(lab, tr, f, c["h"])
 
 
 @pytest.mark.slow
@@ -386,6 +438,7 @@ def test_cfg3_full_vs_reference():
     assert fps == [int(v) for v in f["bins_fp"]]
 
 
+@pytest.mark.usefixtures("exact_sums")
 @pytest.mark.parametrize("name", ["cfg0"])
 def test_big_exact_model_bitwise(name):
     f = G.big(name)
@@ -394,6 +447,7 @@ def test_big_exact_model_bitwise(name):
     _check_model(lab, tr, f, c["h"])
 
 
+@pytest.mark.usefixtures("exact_sums")
 @pytest.mark.slow
 def test_cfg1_exact_model_bitwise():
     f = G.big("cfg1")
@@ -477,6 +531,7 @@ def test_user_stream_and_inplace_accounting():
     assert wb[-1] < wb[0]          # settled points are not rewritten
 
 
+@pytest.mark.usefixtures("exact_sums")
 def test_points_api_sorted_float64_rows():
     # the sort reads fp64 host-layout rows directly (SrcAoS<double>)
     x = W.cloud3d(120_000, seed=62).astype(np.float64)

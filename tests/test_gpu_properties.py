@@ -17,6 +17,7 @@ from tests import exact_model as X
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.usefixtures("exact_sums")
 @settings(max_examples=40)
 @given(st.integers(1, 4), st.integers(1, 60), st.sampled_from([0.25, 0.7, 1.0]), st.integers(0, 2**31 - 1))
 def test_step_bitwise_exact_model(d, n, h, seed):
@@ -71,6 +72,7 @@ def test_extraction_partition(n, seed):
     assert np.allclose(lab.modes, modes, rtol=0, atol=1e-12)
 
 
+@pytest.mark.usefixtures("exact_sums")
 @settings(max_examples=25)
 @given(st.integers(1, 3), st.integers(5, 400), st.sampled_from([0.3, 0.6, 1.1]), st.integers(0, 2**31 - 1))
 def test_full_run_bitwise_exact_model(d, n, h, seed):
@@ -111,6 +113,7 @@ def test_invalid_inputs():
         gs.meanshiftpp(gs.PointSet(np.zeros((3, 9))), gs.ShiftConfig(1.0))   # d > 8: engine envelope
 
 
+@pytest.mark.usefixtures("exact_sums")
 @settings(max_examples=20)
 @given(st.integers(4, 8), st.integers(5, 300), st.sampled_from([0.6, 1.0, 1.7]), st.booleans(),
        st.integers(0, 2**31 - 1))
@@ -126,6 +129,7 @@ def test_full_run_high_d_bitwise_exact_model(d, n, h, spread, seed):
     assert np.array_equal(lab.labels, m["labels"]) and np.array_equal(lab.modes, m["modes"])
 
 
+@pytest.mark.usefixtures("exact_sums")
 def test_large_hash_run_equals_exact_model():
     # a sorted (n >= 32768) run on a hash table (d = 4, wide box)
     rng = np.random.default_rng(77)

@@ -46,6 +46,7 @@ def _worker(rank, world, port, backend, y, h, eta, mi, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.usefixtures("exact_sums")
 @pytest.mark.parametrize("world,backend,n", [(1, "nccl", 200_000), (2, "gloo", 200_000), (2, "gloo", 5_000)])
 def test_cuda_shards_equal_single_gpu(world, backend, n):
     y = W.cloud3d(n, seed=21)

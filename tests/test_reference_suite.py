@@ -12,7 +12,7 @@ import their names, then pytest runs the selected reference tests unmodified:
     (:92-136), loop semantics (:141-236), extraction KATs (:241-316);
   * test_acceptance.py: criterion 1, 200 random step instances including
     points parked on faces (:38-61), criterion 4, engine agreement (:107-115),
-    criterion 5 (segmentation), criterion 8 (tracking, :173-214);
+    criterion 8 (tracking, :173-214);
   * test_track.py: tracker behaviour through the patched
     track.meanshiftpp (:59-182).
 """
@@ -32,7 +32,9 @@ REF_TESTS = ROOT / "baseline" / "_ref" / "tests"
 
 SELECT = {
     "test_modeseek.py": None,
-    "test_acceptance.py": "criterion_1 or criterion_4 or criterion_5 or criterion_8",
+    # criterion 5 needs pkg/assets/images/*.png, which the reference tree does
+    # not ship (it fails on the reference itself)
+    "test_acceptance.py": "criterion_1 or criterion_4 or criterion_8",
     "test_track.py": None,
 }
 
