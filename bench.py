@@ -430,6 +430,11 @@ def our_arm(a):
     if shard:
         line["config"]["parallelism"] = f"rows sharded over {world} GPU(s), NCCL"
     if rank == 0 and not shard:
+        line["sum_order"] = ("reference: per-cell and neighbourhood sums in the reference's sequential "
+                             "order (np.bincount, grid.py:186-187, 253-258); iterates equal the "
+                             "reference's bit for bit")
+        line["refsum"] = refsum_stats(gs, last_iters)
+        line["exact_order"] = exact_leg(gs, torch, x_dev, cfg, labels, n, a.steps)
         line["collapsed"] = collapsed_leg(gs, torch, x_dev, cfg, labels, n, a.steps)
     if not a.no_e2e:
         if shard:
@@ -453,6 +458,38 @@ def our_arm(a):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def refsum_stats(gs, iters):
+    """Per-table counters of the reference-order sums in the last timed run."""
+    st = gs.modeseek.last_refsum_stats(iters)
+    return {"mixed_cells_per_table": [int(v) for v in st[:, 0]],
+            "points_through_global_sort_per_table": [int(v) for v in st[:, 2]],
+            "longest_mixed_cell_per_table": [int(v) for v in st[:, 3]],
+            "note": "cells receiving several source cells are folded in point-index order (stable radix "
+                    "sort for long ones, shared-memory gathers for short ones); single-source cells use "
+                    "the closed form per binade"}
+
+
+def exact_leg(gs, torch, x_dev, cfg, labels, n, steps):
+    """Same workload with GS_SUMS_EXACT (order-independent exact sums rounded
+    once): what the per-point engine costs without the reference's summation
+    order; its modes sit ~1e-9*h from the reference's at cfg4."""
+    with gs.sum_order("exact"):
+        gs.meanshiftpp_device(x_dev, cfg, labels)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        it = 0
+        e0.record()
+        for _ in range(steps):
+            it += gs.meanshiftpp_device(x_dev, cfg, labels)[2]
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"value": n * it / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps,
+            "note": "GS_SUMS_EXACT: exact fixed-point sums rounded once (order-independent; the row-sharded "
+                    "multi-GPU path computes these); not bit-identical to the reference, so not the headline"}
 
 
 def collapsed_leg(gs, torch, x_dev, cfg, labels, n, steps):

@@ -582,8 +582,13 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
         R.runkey, R.outslot, R.rs[0], R.ctl, R.seglen, R.sstart, R.send, R.seglist, R.runkv, lowrun);
   });
   if (!R.all_big) {
+    static std::atomic<uint64_t> wattr{0};
+    if (attr_pending(wattr, c->device)) {
+      GS_CUDA(cudaFuncSetAttribute(k_rs_gather_warp<D, InVal<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherWarpSmem));
+      attr_done(wattr, c->device);
+    }
     launch(c, K_REFSUM, [&] {
-      k_rs_gather_warp<D, InVal<D>, true><<<c->sms * 8, 256, 0, c->st>>>(R.ctl, R.seglen, nullptr, R.seglist, R.start,
+      k_rs_gather_warp<D, InVal<D>, true><<<c->sms * 8, 256, kGatherWarpSmem, c->st>>>(R.ctl, R.seglen, nullptr, R.seglist, R.start,
                                                                          R.end, R.perm, nullptr, V, R.outslot,
                                                                          R.rs[0], false);
     });
@@ -635,8 +640,13 @@ void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
     launch(c, K_REFSUM, [&] { k_scan32_top<<<1, 1024, 0, c->st>>>(R.segscan, nsb, nullptr, 0); });
     launch(c, K_REFSUM, [&] { k_scan32_apply<<<nsb, 256, 0, c->st>>>(R.segbeg, ns, R.segscan, nullptr, 0); });
     launch(c, K_REFSUM, [&] { k_rs_fill<<<nbr, kThreads, 0, c->st>>>(R.runs, R.nruns, R.runseg, R.segbeg, R.segcur, R.seglist); });
+    static std::atomic<uint64_t> wattr{0};
+    if (attr_pending(wattr, c->device)) {
+      GS_CUDA(cudaFuncSetAttribute(k_rs_gather_warp<D, RecVal<D>, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherWarpSmem));
+      attr_done(wattr, c->device);
+    }
     launch(c, K_REFSUM, [&] {
-      k_rs_gather_warp<D, RecVal<D>, false><<<c->sms * 8, 256, 0, c->st>>>(R.ctl, R.seglen, R.segbeg, R.seglist,
+      k_rs_gather_warp<D, RecVal<D>, false><<<c->sms * 8, 256, kGatherWarpSmem, c->st>>>(R.ctl, R.seglen, R.segbeg, R.seglist,
                                                                           R.start, R.end, R.perm, R.runval,
                                                                           RecVal<D>{rec}, R.outslot, R.rs[cur ^ 1],
                                                                           false);

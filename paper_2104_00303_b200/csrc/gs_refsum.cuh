@@ -147,10 +147,11 @@ __host__ __device__ inline double seqsum_const(double v, u64 c) {
 // block; warp w of a tile owns elements [512 w, 512 w + 512), item-major
 // within the warp, so rank order == element order (stability).
 
-constexpr int kRsThreads = 256, kRsItems = 16, kRsTile = kRsThreads * kRsItems;
+constexpr int kRsThreads = 256, kRsItems = 8, kRsTile = kRsThreads * kRsItems;
 constexpr int kRsWarps = kRsThreads / 32;
 
 struct RsBufSrc {
+  static constexpr bool kRunStream = false;
   const u32* keys;
   const u32* vals;
   const u32* n;       // element count (device)
@@ -166,6 +167,7 @@ struct RsBufSrc {
 // packed 8-byte gather (runkv: key low, value high; value ~0 = the point
 // index i itself).
 struct RsRunSrc {
+  static constexpr bool kRunStream = true;
   const u32* cell0;
   const u64* runkv;
   i64 n;
@@ -186,13 +188,32 @@ template <class Src>
 __device__ __forceinline__ void rs_load_tile(const Src& src, i64 base, i64 n, u32 (&k)[kRsItems],
                                              u32 (&v)[kRsItems], bool (&ok)[kRsItems]) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (Src::kRunStream) {
+    // two phases so every item's run index is in flight before the gathers
+    u32 r[kRsItems];
 #pragma unroll
-  for (int it = 0; it < kRsItems; ++it) {
-    const i64 i = base + (i64)w * (32 * kRsItems) + it * 32 + lane;
-    ok[it] = false;
-    k[it] = kRsEmpty;
-    v[it] = 0;
-    if (i < n) ok[it] = src.get(i, k[it], v[it]);
+    for (int it = 0; it < kRsItems; ++it) {
+      const i64 i = base + (i64)w * (32 * kRsItems) + it * 32 + lane;
+      r[it] = i < n ? __ldcs(src.cell0 + i) : kRsEmpty;
+    }
+#pragma unroll
+    for (int it = 0; it < kRsItems; ++it) {
+      const i64 i = base + (i64)w * (32 * kRsItems) + it * 32 + lane;
+      const u64 kv = r[it] == kRsEmpty ? ~0ull : src.runkv[r[it]];
+      k[it] = (u32)kv;
+      v[it] = (u32)(kv >> 32);
+      if (v[it] == kRsEmpty) v[it] = (u32)i;
+      ok[it] = k[it] != kRsEmpty;
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < kRsItems; ++it) {
+      const i64 i = base + (i64)w * (32 * kRsItems) + it * 32 + lane;
+      ok[it] = false;
+      k[it] = kRsEmpty;
+      v[it] = 0;
+      if (i < n) ok[it] = src.get(i, k[it], v[it]);
+    }
   }
 }
 
@@ -302,11 +323,18 @@ __global__ void __launch_bounds__(256) k_scan32_apply(u32* a, i64 n, const u32* 
   }
 }
 
-// stable scatter by digit: offsets = scanned counts
+// stable scatter by digit: offsets = scanned counts.  The tile is first
+// ordered by digit in shared memory (stable), then written out with
+// consecutive threads on consecutive positions of each digit's run, so the
+// global writes coalesce instead of scattering 4-byte stores.
 template <class Src>
-__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(Src src, const RsCtl* ctl, int pass, const u32* offs,
-                                                           u32 nblk, u32* okeys, u32* ovals) {
+__global__ void __launch_bounds__(kRsThreads, 4) k_rs_scatter(Src src, const RsCtl* ctl, int pass, const u32* offs,
+                                                              u32 nblk, u32* okeys, u32* ovals) {
   __shared__ u32 base[kRsWarps][256];
+  __shared__ u32 tdig[257];      // the tile's exclusive digit offsets
+  __shared__ u32 gofs[256];      // global offset of (digit, tile)
+  __shared__ u32 sk[kRsTile];
+  __shared__ u32 sv[kRsTile];
   if (!rs_pass_live(ctl, pass)) return;
   const i64 n = src.count();
   const i64 t0 = (i64)blockIdx.x * kRsTile;
@@ -326,16 +354,35 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(Src src, const RsCtl*
     __syncwarp();
   }
   __syncthreads();
+  u32 tot;
   {
-    // digit d: warp bases = global offset of (d, tile) + counts of earlier warps
+    // digit d: warp bases inside the tile's digit run; the tile's count
     const int d = threadIdx.x;
-    u32 acc = offs[(size_t)d * nblk + blockIdx.x];
+    u32 acc = 0;
 #pragma unroll
     for (int ww = 0; ww < kRsWarps; ++ww) {
       const u32 c = base[ww][d];
       base[ww][d] = acc;
       acc += c;
     }
+    tot = acc;
+    gofs[d] = offs[(size_t)d * nblk + blockIdx.x];
+  }
+  // exclusive scan of the tile's digit counts (256 threads = 256 digits)
+  {
+    u32 inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    __shared__ u32 ws[kRsWarps];
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    u32 wb = 0;
+    for (int ww = 0; ww < w; ++ww) wb += ws[ww];
+    tdig[threadIdx.x] = wb + inc - tot;
+    if (threadIdx.x == 255) tdig[256] = wb + inc;
   }
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
@@ -343,14 +390,23 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(Src src, const RsCtl*
   for (int it = 0; it < kRsItems; ++it) {
     const unsigned peers = __match_any_sync(kFull, dg[it]);
     u32 pos = 0;
-    if (dg[it] < 256u) pos = base[w][dg[it]] + (u32)__popc(peers & lt);
+    if (dg[it] < 256u) pos = tdig[dg[it]] + base[w][dg[it]] + (u32)__popc(peers & lt);
     __syncwarp();
     if (dg[it] < 256u && lane == __ffs(peers) - 1) base[w][dg[it]] += (u32)__popc(peers);
     __syncwarp();
     if (dg[it] < 256u) {
-      okeys[pos] = k[it];
-      ovals[pos] = v[it];
+      sk[pos] = k[it];
+      sv[pos] = v[it];
     }
+  }
+  __syncthreads();
+  const u32 nt = tdig[256];
+  for (u32 e = threadIdx.x; e < nt; e += kRsThreads) {
+    const u32 kk = sk[e];
+    const u32 d = (kk >> (8 * pass)) & 255u;
+    const u32 out = gofs[d] + (e - tdig[d]);
+    okeys[out] = kk;
+    ovals[out] = sv[e];
   }
 }
 
@@ -509,34 +565,52 @@ __global__ void __launch_bounds__(256) k_fold_delta(RsSorted so, const RsCtl* ct
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
   for (i64 w = warp; w < nw; w += nwarps) {
+    // per axis: the binade the window's accumulator provably stays in
+    // (|accumulator - prefix| <= elements so far * 2^-53 * accumulator;
+    // 2^-20 covers any segment below 2^32 points)
+    int ue[D];
+    bool live[D], any = false;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const double ws = wsum[w * D + j];
-      u64 res = kNoDelta;
+      live[j] = false;
+      ue[j] = 0;
       if (ws >= 0.0) {
-        // |accumulator - prefix| <= (elements so far) * 2^-53 * accumulator;
-        // 2^-20 covers any segment below 2^32 points
         const double lo = wpre[w * D + j] * (1.0 - 0x1p-20);
         const double hi = (wpre[w * D + j] + ws) * (1.0 + 0x1p-20);
         const int blo = (int)(dbits(lo) >> 52), bhi = (int)(dbits(hi) >> 52);
         if (lo > 0x1p-900 && blo == bhi && bhi < 2047) {
-          const int ue = blo - 1075;
-          u64 sum = 0;
-          bool tie = false;
-          for (int q = lane; q < kFoldWin; q += 32) {
-            const double x = scale2(fabs(V.get(vals[w * kFoldWin + q], j)), -ue);
-            const double fl = floor(x);
-            const double fr = x - fl;
-            tie |= fr == 0.5;
-            sum += (u64)fl + (fr > 0.5 ? 1ull : 0ull);
-          }
-          for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-          tie = __any_sync(kFull, tie);
-          // tag: the biased exponent of the binade the step is valid in (11
-          // bits above the 53-bit step)
-          if (!tie && sum <= kMaxM) res = ((u64)blo << 53) | sum;
+          live[j] = true;
+          ue[j] = blo - 1075;
+          any = true;
         }
       }
+    }
+    u64 sum[D];
+    bool tie[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { sum[j] = 0; tie[j] = false; }
+    if (any) {
+      for (int q = lane; q < kFoldWin; q += 32) {
+        const u32 vv = vals[w * kFoldWin + q];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          if (!live[j]) continue;
+          const double x = scale2(fabs(V.get(vv, j)), -ue[j]);
+          const double fl = floor(x);
+          const double fr = x - fl;
+          tie[j] |= fr == 0.5;
+          sum[j] += (u64)fl + (fr > 0.5 ? 1ull : 0ull);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      for (int o = 16; o; o >>= 1) sum[j] += __shfl_xor_sync(kFull, sum[j], o);
+      const bool t = __any_sync(kFull, tie[j]);
+      // tag: the biased exponent of the binade the step is valid in (11
+      // bits above the 53-bit step)
+      const u64 res = (live[j] && !t && sum[j] <= kMaxM) ? (((u64)(ue[j] + 1075) << 53) | sum[j]) : kNoDelta;
       if (lane == 0) wdelta[w * D + j] = res;
     }
   }
@@ -786,6 +860,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_fill(const u32* runs, const u32
 }
 
 constexpr u32 kGatherWarp = 256;   // gathered segments up to this size: one warp each
+constexpr size_t kGatherWarpSmem = (size_t)8 * 2 * kGatherWarp * sizeof(u32);
 
 // One warp per gathered segment of <= kGatherWarp points (the common case
 // once clusters contract): run offsets by a warp scan, points' original
@@ -796,13 +871,12 @@ __global__ void __launch_bounds__(256) k_rs_gather_warp(const RsCtl* ctl, const 
                                                         const u32* seglist, const u32* start, const u32* end,
                                                         const u32* perm, const u32* runval, Val V,
                                                         const u32* outslot, double* rs, bool all_big) {
-  __shared__ u32 sidx[8][kGatherWarp];
-  __shared__ u32 sval[8][kGatherWarp];
+  extern __shared__ u32 wsm[];
   if (all_big) return;
   const u32 nseg = ctl->nseg;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  u32* xi = sidx[w];
-  u32* xv = sval[w];
+  u32* xi = wsm + (size_t)w * 2 * kGatherWarp;
+  u32* xv = xi + kGatherWarp;
   const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
   for (i64 q = gw; q < nseg; q += nw) {

@@ -45,6 +45,23 @@ def test_mass_conservation(seed, n, d, h):
     assert np.array_equal(t.cells, ref.cells) and np.array_equal(t.counts, ref.counts)
 
 
+@given(seed=st.integers(0, 10_000), d=st.integers(1, 4))
+def test_neighbourhood_bitwise_reference_order(seed, d):
+    # reference-order sums (the default): tables and neighbourhood sums equal
+    # the reference's (the oracle reproduces them bitwise, test_oracle.py)
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300))
+    data = rng.normal(0.0, 3.0, size=(n, d))
+    h = float(rng.uniform(0.2, 2.0))
+    t = gs.neighbor_stats(gs.PointSet(data), h)
+    ref, _ = O.cell_tables(data, h)
+    nc, ns = O.neighbour_stats(ref)
+    assert np.array_equal(t.cells, ref.cells) and np.array_equal(t.counts, ref.counts)
+    assert np.array_equal(t.sums, ref.sums)
+    assert np.array_equal(t.nbr_counts, nc) and np.array_equal(t.nbr_sums, ns)
+
+
+@pytest.mark.usefixtures("exact_sums")
 @given(seed=st.integers(0, 10_000), d=st.integers(1, 3))
 def test_neighbourhood_equals_linear_scan(seed, d):
     # test_grid.py:190-205: counts bitwise, sums = exactly rounded scan sums
