@@ -129,6 +129,13 @@ GS_API int gs_segment_image(gs_ctx* ctx, const uint8_t* pixels, int32_t height, 
 #define GS_SUMS_EXACT 1
 GS_API int gs_ctx_set_option(gs_ctx* ctx, int32_t option, int64_t value);
 
+/* Mean colours (k, 3) of the segments of the last gs_segment_image on this
+ * context: SegmentMap.mean_colors as segment_map_from_labeling computes them
+ * (segment.py:109-117: np.bincount sums of the uint8 colours per label /
+ * counts).  The per-label sums are accumulated on the device as integers, so
+ * the quotients equal the reference's bit for bit. */
+GS_API int gs_fetch_mean_colors(gs_ctx* ctx, double* colors_out, int64_t cap_rows);
+
 /* Modes (k, d) of the last run on this context (Labeling.modes). */
 GS_API int gs_fetch_modes(gs_ctx* ctx, double* modes_out, int64_t cap_rows);
 

@@ -13,7 +13,8 @@ from .grid import (CellTables, PointSet, bin_point, bin_points, build_cell_table
 from .modeseek import (ENGINES, Labeling, ShiftConfig, ShiftTrace, extract_clusters, install,
                        set_sum_order, sum_order,
                        meanshiftpp, meanshiftpp_device, meanshiftpp_points, meanshiftpp_step)
-from .segment import Image, SegmentMap, image_to_features, segment_image, segment_pixels
+from .segment import (Image, SegmentMap, image_to_features, segment_image, segment_map_from_labeling,
+                      segment_pixels)
 from .track import (BinSet, TrackState, Window, cluster_window, init_tracker, neighborhood,
                     track_frame, track_sequence)
 
@@ -22,6 +23,7 @@ __all__ = [
     "ShiftConfig", "ShiftTrace", "TrackState", "Window", "bin_point", "bin_points",
     "build_cell_tables", "cluster_window", "extract_clusters", "image_to_features",
     "init_tracker", "install", "set_sum_order", "sum_order", "meanshiftpp", "meanshiftpp_device", "meanshiftpp_points", "meanshiftpp_step",
-    "neighbor_aggregate", "neighbor_stats", "neighborhood", "segment_batch", "segment_image", "segment_pixels",
+    "neighbor_aggregate", "neighbor_stats", "neighborhood", "segment_batch", "segment_image",
+    "segment_map_from_labeling", "segment_pixels",
     "track_frame", "track_sequence",
 ]

@@ -24,6 +24,8 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr",
 ]
+# development only: e.g. GS_NVCC_EXTRA="-DGS_ONLY_D=3" builds one dimension (8x faster)
+NVCC_FLAGS += os.environ.get("GS_NVCC_EXTRA", "").split()
 
 
 def _nvcc() -> str:

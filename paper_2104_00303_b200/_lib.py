@@ -40,6 +40,7 @@ SIGNATURES = {
     "gs_segment_image": (C.c_int, [_P, _P, _i32, _i32, _i32, _f64, _f64, _f64, _i32, _P, _P, _P,
                                    _P, _P]),
     "gs_fetch_modes": (C.c_int, [_P, _P, _i64]),
+    "gs_fetch_mean_colors": (C.c_int, [_P, _P, _i64]),
     "gs_ctx_set_option": (C.c_int, [_P, _i32, _i64]),
     "gs_fetch_trace": (C.c_int, [_P, _P, _P, _i32]),
     "gs_fetch_shift_bytes": (C.c_int, [_P, _P, _i32]),

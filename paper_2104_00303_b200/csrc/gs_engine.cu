@@ -103,6 +103,13 @@ struct RsRun {
   void* tag[2] = {nullptr, nullptr};   // per table buffer: Rec<D> the slot's closed form came from
   u32* stats = nullptr;         // per table: 5 counters (k_rs_stats)
   int stats_rows = 0;
+  // index-ordered point lists of the cells (RsLists): per table buffer the
+  // list of each slot, source chains of the mixed targets, the arena (perm
+  // first) and its fill mark
+  u64* lst[2] = {nullptr, nullptr};
+  u32 *shead = nullptr, *snext = nullptr, *segdone = nullptr, *ctalist = nullptr;
+  u64 arena_cap = 0;
+  unsigned long long* arena_top = nullptr;
 };
 
 struct gs_ctx {
@@ -123,6 +130,8 @@ struct gs_ctx {
   int d_last = 0;
   int64_t k_last = 0;
   std::vector<double> modes_host;
+  std::vector<double> colors_host;      // (k, 3) mean colours of the last gs_segment_image
+  Buf colsum;
   std::vector<int64_t> iter_k;
   std::vector<uint64_t> iter_fp;
   std::vector<int64_t> track_bins;
@@ -163,7 +172,8 @@ struct gs_ctx {
   bool it_sorted = false, it_valid = false;
   Buf rsb[2], rs_nsrc, rs_mid, rs_out, rs_rc[2], rs_rkey, rs_rval, rs_k[2], rs_v[2], rs_cnt, rs_scan,
       rs_start, rs_end, rs_wsum, rs_wpre, rs_wdelta, rs_ctl, rs_cell0, rs_runs, rs_seglen, rs_segbeg,
-      rs_segcur, rs_seglist, rs_runseg, rs_segscan, rs_runkv, rs_tag[2], rs_stats, rs_lowrun;
+      rs_segcur, rs_seglist, rs_runseg, rs_segscan, rs_runkv, rs_tag[2], rs_stats, rs_lowrun, rs_lst[2],
+      rs_shead, rs_snext, rs_segdone, rs_atop, rs_ctalist;
   RsRun rsr;
 };
 
@@ -424,6 +434,10 @@ struct SortInfo {
 // (gs_refsum.cuh).  rs_alloc sizes the buffers of one run; rs_first builds
 // the first table's sums, rs_next those of table t+1 right after k_derive.
 
+// perm (n entries) plus room for the merged lists of later tables (list
+// offsets are 32-bit; a full arena only costs speed)
+inline u64 arena_entries(int64_t n) { return std::min<u64>(4ull * (u64)n, 0xfffffff0ull); }
+
 RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 segcap, int max_iters = 1) {
   RsRun& R = c->rsr;
   R.on = true;
@@ -472,6 +486,14 @@ RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 se
   GS_CUDA(cudaMemsetAsync(R.stats, 0, 20ull * R.stats_rows, c->st));
   GS_CUDA(cudaMemsetAsync(R.nsrc, 0, sizeof(u32) * p.slots, c->st));
   GS_CUDA(cudaMemsetAsync(R.mid, 0xff, sizeof(u32) * p.slots, c->st));
+  for (int b = 0; b < 2; ++b) R.lst[b] = ensure<u64>(c, c->rs_lst[b], p.slots);
+  R.shead = ensure<u32>(c, c->rs_shead, p.slots);
+  R.snext = ensure<u32>(c, c->rs_snext, p.slots);
+  R.segdone = ensure<u32>(c, c->rs_segdone, R.segcap);
+  R.ctalist = ensure<u32>(c, c->rs_ctalist, R.segcap);
+  R.arena_top = reinterpret_cast<unsigned long long*>(ensure<u64>(c, c->rs_atop, 1));
+  R.arena_cap = 0;
+  GS_CUDA(cudaMemsetAsync(R.shead, 0xff, sizeof(u32) * p.slots, c->st));
   return R;
 }
 
@@ -480,6 +502,7 @@ RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 se
 template <class Src0>
 void rs_sort(gs_ctx* c, RsRun& R, const Src0& src0) {
   const u32 nb = R.nblk;
+  const u32 ng = std::min<u32>(nb, (u32)c->sms * 16);   // blocks loop over the tiles
   const int64_t ncnt = 256ll * nb;
   const int nsb = (int)((ncnt + kScan32Chunk - 1) / kScan32Chunk);
   for (int pass = 0; pass < R.maxpasses; ++pass) {
@@ -487,11 +510,11 @@ void rs_sort(gs_ctx* c, RsRun& R, const Src0& src0) {
     u32* ov = R.v[pass & 1];
     auto go = [&](const auto& src) {
       using S = std::decay_t<decltype(src)>;
-      launch(c, K_REFSUM, [&] { k_rs_count<S><<<nb, kRsThreads, 0, c->st>>>(src, R.ctl, pass, R.cnt, nb); });
+      launch(c, K_REFSUM, [&] { k_rs_count<S><<<ng, kRsThreads, 0, c->st>>>(src, R.ctl, pass, R.cnt, nb); });
       launch(c, K_REFSUM, [&] { k_scan32_reduce<<<nsb, 256, 0, c->st>>>(R.cnt, ncnt, R.scan, R.ctl, pass); });
       launch(c, K_REFSUM, [&] { k_scan32_top<<<1, 1024, 0, c->st>>>(R.scan, nsb, R.ctl, pass); });
       launch(c, K_REFSUM, [&] { k_scan32_apply<<<nsb, 256, 0, c->st>>>(R.cnt, ncnt, R.scan, R.ctl, pass); });
-      launch(c, K_REFSUM, [&] { k_rs_scatter<S><<<nb, kRsThreads, 0, c->st>>>(src, R.ctl, pass, R.cnt, nb, ok, ov); });
+      launch(c, K_REFSUM, [&] { k_rs_scatter<S><<<ng, kRsThreads, 0, c->st>>>(src, R.ctl, pass, R.cnt, nb, ok, ov); });
     };
     if (pass == 0)
       go(src0);
@@ -539,6 +562,10 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
     R.end = si->end;
     R.perm = si->perm;
     R.all_big = si->perm == nullptr;
+    if (si->perm) {
+      R.arena_cap = arena_entries(n);
+      launch(c, K_REFSUM, [&] { k_rs_set64<<<1, 1, 0, c->st>>>(R.arena_top, (unsigned long long)n); });
+    }
   } else {
     u32* c0 = ensure<u32>(c, c->rs_cell0, (size_t)n);
     launch(c, K_REFSUM, [&] { k_rs_cell0<D, Tab><<<blocks_for(c, n), kThreads, 0, c->st>>>(ys, n, p.g, tabs[0], c0); });
@@ -579,7 +606,8 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
   launch(c, K_REFSUM, [&] {
     k_rs_first<D, Tab><<<blocks_for(c, (int64_t)p.list_cap), kThreads, 0, c->st>>>(
         p.g, tabs[0], R.runs, R.nruns, si ? si->start : nullptr, ys, si != nullptr, !R.all_big, lb, R.rc[0],
-        R.runkey, R.outslot, R.rs[0], R.ctl, R.seglen, R.sstart, R.send, R.seglist, R.runkv, lowrun);
+        R.runkey, R.outslot, R.rs[0], R.ctl, R.seglen, R.sstart, R.send, R.seglist, R.runkv, lowrun,
+        R.arena_cap ? R.lst[0] : nullptr);
   });
   if (!R.all_big) {
     static std::atomic<uint64_t> wattr{0};
@@ -590,7 +618,7 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
     launch(c, K_REFSUM, [&] {
       k_rs_gather_warp<D, InVal<D>, true><<<c->sms * 8, 256, kGatherWarpSmem, c->st>>>(R.ctl, R.seglen, nullptr, R.seglist, R.start,
                                                                          R.end, R.perm, nullptr, V, R.outslot,
-                                                                         R.rs[0], false);
+                                                                         R.rs[0], false, RsLists{});
     });
     static std::atomic<uint64_t> attr{0};
     if (attr_pending(attr, c->device)) {
@@ -600,7 +628,7 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
     launch(c, K_REFSUM, [&] {
       k_rs_gather<D, InVal<D>, true><<<c->sms * 2, 256, kGatherSmem, c->st>>>(R.ctl, R.seglen, nullptr, R.seglist, R.start,
                                                                     R.end, R.perm, nullptr, V, R.outslot, R.rs[0],
-                                                                    false);
+                                                                    false, RsLists{}, nullptr);
     });
   }
   launch(c, K_REFSUM, [&] { k_rs_passes<<<1, 1, 0, c->st>>>(R.ctl); });
@@ -620,12 +648,29 @@ void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
   GS_CUDA(cudaMemsetAsync(R.segbeg, 0, sizeof(u32) * (R.segcap + 1), c->st));
   GS_CUDA(cudaMemsetAsync(R.segcur, 0, sizeof(u32) * R.segcap, c->st));
   const int64_t items = Tab::kDense ? (int64_t)p.slots : (int64_t)p.list_cap;
+  const RsLists L{R.arena_cap != 0, R.lst[cur], R.lst[cur ^ 1], R.shead, R.snext, R.segdone,
+                  const_cast<u32*>(R.perm), R.arena_cap, R.arena_top};
   launch(c, K_REFSUM, [&] {
     k_rs_classify<D, Tab><<<blocks_for(c, items), kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur, t,
                                                                         R.nsrc, R.mid, R.outslot, R.rs[cur ^ 1], R.ctl,
                                                                         R.seglen, R.sstart, R.send, R.all_big,
-                                                                        static_cast<Rec<D>*>(R.tag[cur ^ 1]));
+                                                                        static_cast<Rec<D>*>(R.tag[cur ^ 1]), L, R.ctalist);
   });
+  if (L.on) {
+    // mixed targets whose sources carry point lists: rank-merge + fold
+    static std::atomic<uint64_t> mattr{0};
+    if (attr_pending(mattr, c->device)) {
+      GS_CUDA(cudaFuncSetAttribute(k_rs_merge_warp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)merge_warp_smem(D)));
+      GS_CUDA(cudaFuncSetAttribute(k_rs_merge<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)merge_smem(D)));
+      attr_done(mattr, c->device);
+    }
+    launch(c, K_REFSUM, [&] {
+      k_rs_merge_warp<D><<<c->sms * 8, 256, merge_warp_smem(D), c->st>>>(R.ctl, R.seglen, R.outslot, rec, L, R.rs[cur ^ 1]);
+    });
+    launch(c, K_REFSUM, [&] {
+      k_rs_merge<D><<<c->sms * 2, 256, merge_smem(D), c->st>>>(R.ctl, R.seglen, R.outslot, rec, L, R.rs[cur ^ 1], R.ctalist);
+    });
+  }
   const int nbr = blocks_for(c, (int64_t)p.list_cap);
   launch(c, K_REFSUM, [&] {
     k_rs_runs<D, Tab><<<nbr, kThreads, 0, c->st>>>(R.runs, R.nruns, R.rc[cur], R.rc[cur ^ 1], rec, tabs[cur ^ 1], R.mid,
@@ -649,7 +694,7 @@ void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
       k_rs_gather_warp<D, RecVal<D>, false><<<c->sms * 8, 256, kGatherWarpSmem, c->st>>>(R.ctl, R.seglen, R.segbeg, R.seglist,
                                                                           R.start, R.end, R.perm, R.runval,
                                                                           RecVal<D>{rec}, R.outslot, R.rs[cur ^ 1],
-                                                                          false);
+                                                                          false, L);
     });
     static std::atomic<uint64_t> attr{0};
     if (attr_pending(attr, c->device)) {
@@ -659,14 +704,14 @@ void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
     launch(c, K_REFSUM, [&] {
       k_rs_gather<D, RecVal<D>, false><<<c->sms * 2, 256, kGatherSmem, c->st>>>(R.ctl, R.seglen, R.segbeg, R.seglist, R.start,
                                                                      R.end, R.perm, R.runval, RecVal<D>{rec},
-                                                                     R.outslot, R.rs[cur ^ 1], false);
+                                                                     R.outslot, R.rs[cur ^ 1], false, L, R.ctalist);
     });
   }
   launch(c, K_REFSUM, [&] { k_rs_passes<<<1, 1, 0, c->st>>>(R.ctl); });
   rs_sort(c, R, RsRunSrc{R.cell0, R.runkv, R.n});
   rs_fold<D>(c, R, RecVal<D>{rec}, R.rs[cur ^ 1]);
   if (t + 1 < R.stats_rows) launch(c, K_REFSUM, [&] { k_rs_stats<<<1, 1, 0, c->st>>>(R.ctl, R.stats + 5 * (t + 1)); });
-  launch(c, K_REFSUM, [&] { k_rs_unmark<<<blocks_for(c, (int64_t)R.segcap), kThreads, 0, c->st>>>(R.outslot, R.ctl, R.mid); });
+  launch(c, K_REFSUM, [&] { k_rs_unmark<<<blocks_for(c, (int64_t)R.segcap), kThreads, 0, c->st>>>(R.outslot, R.ctl, R.mid, L.on ? R.shead : nullptr); });
   GS_CUDA(cudaMemsetAsync(R.nsrc, 0, sizeof(u32) * p.slots, c->st));
 }
 
@@ -1123,7 +1168,8 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
   si.runs = ensure<u32>(c, c->runlist, p.list_cap);
   si.cell0 = ensure<u32>(c, c->cell0, (size_t)n);
   si.slots0 = p.slots;
-  si.perm = c->exact_sums ? nullptr : ensure<u32>(c, c->perm, (size_t)n);
+  // reference-order sums: perm, followed by the arena of merged point lists
+  si.perm = c->exact_sums ? nullptr : ensure<u32>(c, c->perm, (size_t)arena_entries(n));
   si.runroot = off;   // the cursors are dead once the scatter is done...
   si.end = off;       // ...except as run ends, read (collapsed mode) before runroot is written
   GS_CUDA(cudaMemsetAsync(si.minidx, 0xff, p.slots * sizeof(u32), c->st));
@@ -1665,6 +1711,15 @@ void shard_finish_d(gs_ctx* c, ShardState* sh, const long long* minima, int64_t*
   extract_finish<D>(c, sh->p, tabs.dn, yf, sh->n, e, labels_dev, sp);
 }
 
+// GS_ONLY_D (development builds: nvcc -DGS_ONLY_D=3) instantiates one
+// dimension only; the shipped library is built without it.
+#ifdef GS_ONLY_D
+#define GS_DISPATCH(d, CALL)                                                    \
+  switch (d) {                                                                  \
+    case GS_ONLY_D: { constexpr int DD = GS_ONLY_D; CALL; } break;               \
+    default: fail(GS_EUNSUPPORTED, "development build: one dimension only");      \
+  }
+#else
 #define GS_DISPATCH(d, CALL)                                                    \
   switch (d) {                                                                  \
     case 1: { constexpr int DD = 1; CALL; } break;                               \
@@ -1677,6 +1732,7 @@ void shard_finish_d(gs_ctx* c, ShardState* sh, const long long* minima, int64_t*
     case 8: { constexpr int DD = 8; CALL; } break;                               \
     default: fail(GS_EUNSUPPORTED, "unsupported d");                              \
   }
+#endif
 
 // ===================================================================== C ABI
 
@@ -1717,7 +1773,7 @@ void gs_ctx_destroy(gs_ctx* c) {
   Buf* bufs[] = {&c->x_stage, &c->y[0], &c->y[1], &c->ent[0], &c->ent[1], &c->keys[0], &c->keys[1],
                  &c->list[0], &c->list[1], &c->targets, &c->partials, &c->par, &c->first, &c->aux,
                  &c->roots, &c->root_first, &c->ranks, &c->modes, &c->labels, &c->mv_hist,
-                 &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->track,
+                 &c->fp_hist, &c->k_hist, &c->stats, &c->ctrl, &c->perm, &c->colsum, &c->track,
                  &c->track_out, &c->bitmaps, &c->scan, &c->runoff, &c->runstart, &c->runmin,
                  &c->runlist, &c->cell0, &c->stage, &c->runposb, &c->runcntb, &c->bkcnt, &c->bktot, &c->bocc, &c->bmask, &c->wr_hist};
   for (Buf* b : bufs)
@@ -1727,7 +1783,8 @@ void gs_ctx_destroy(gs_ctx* c) {
                   &c->rs_scan, &c->rs_start, &c->rs_end, &c->rs_wsum, &c->rs_wpre, &c->rs_wdelta, &c->rs_ctl,
                   &c->rs_cell0, &c->rs_runs, &c->rs_seglen, &c->rs_segbeg, &c->rs_segcur, &c->rs_seglist,
                   &c->rs_runseg, &c->rs_segscan, &c->rs_runkv, &c->rs_tag[0], &c->rs_tag[1], &c->rs_stats,
-                  &c->rs_lowrun};
+                  &c->rs_lowrun, &c->rs_lst[0], &c->rs_lst[1], &c->rs_shead, &c->rs_snext, &c->rs_segdone,
+                  &c->rs_atop, &c->rs_ctalist};
   for (Buf* b : rbufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
@@ -1835,10 +1892,34 @@ int gs_segment_image(gs_ctx* c, const uint8_t* pixels, int32_t height, int32_t w
       HostLabelRequest req(c);
       r = run_engine(c, in, n, d, h, eta, max_iters, dl, movement_out);
     }
-    deliver_labels(c, dl, labels_out, n);
+    // per-segment colour sums on device while the labels travel
+    u64* cs = ensure<u64>(c, c->colsum, (size_t)r.k * 4);
+    GS_CUDA(cudaMemsetAsync(cs, 0, sizeof(u64) * 4 * (size_t)r.k, c->st));
+    const bool by_cell = c->labels_on_host;
+    launch(c, K_LABELS, [&] {
+      k_label_colors<<<blocks_for(c, n), kThreads, 0, c->st>>>(dp, n, by_cell ? c->cell0_dev : nullptr,
+                                                              by_cell ? static_cast<const u32*>(c->slotlab.p) : nullptr,
+                                                              reinterpret_cast<const i64*>(dl), cs);
+    });
+    std::vector<u64> hs((size_t)r.k * 4);
+    GS_CUDA(cudaMemcpyAsync(hs.data(), cs, sizeof(u64) * hs.size(), cudaMemcpyDeviceToHost, c->st));
+    deliver_labels(c, dl, labels_out, n);   // synchronises the stream
+    c->xfer_d2h += (int64_t)(sizeof(u64) * hs.size());
+    c->colors_host.resize((size_t)r.k * 3);
+    for (int64_t q = 0; q < r.k; ++q)
+      for (int ch = 0; ch < 3; ++ch)
+        c->colors_host[q * 3 + ch] = (double)hs[q * 4 + ch] / (double)hs[q * 4 + 3];
     if (k_out) *k_out = r.k;
     if (iters_out) *iters_out = r.iters;
     if (converged_out) *converged_out = r.converged;
+  });
+}
+
+int gs_fetch_mean_colors(gs_ctx* c, double* colors_out, int64_t cap_rows) {
+  return guarded(c, [&] {
+    if (c->colors_host.empty()) fail(GS_EINVAL, "no segmentation on this context yet");
+    if (cap_rows * 3 < (int64_t)c->colors_host.size()) fail(GS_EINVAL, "mean colour buffer too small");
+    memcpy(colors_out, c->colors_host.data(), sizeof(double) * c->colors_host.size());
   });
 }
 

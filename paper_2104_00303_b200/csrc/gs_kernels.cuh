@@ -1954,6 +1954,39 @@ __global__ void __launch_bounds__(kThreads) k_slot_labels(const u32* __restrict_
   }
 }
 
+// Per-segment colour sums and pixel counts of a segmentation
+// (segment_map_from_labeling, segment.py:109-117): pixel i carries label
+// slotlab[cell0[i]] (host label delivery) or labels[i].  uint8 colours sum
+// exactly in integers, so the means (sum / count in fp64) equal np.bincount's.
+// Lanes of a warp with the same label combine before the atomics
+// (neighbouring pixels mostly share a segment).  out: [label][4] = r, g, b, n.
+__global__ void __launch_bounds__(kThreads) k_label_colors(const unsigned char* __restrict__ pix, i64 n,
+                                                           const u32* __restrict__ cell0,
+                                                           const u32* __restrict__ slotlab,
+                                                           const i64* __restrict__ labels, u64* out) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (i64 i0 = (i64)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const i64 i = i0 + lane;
+    u32 lab = 0xffffffffu, r = 0, g = 0, b = 0;
+    if (i < n) {
+      lab = cell0 ? slotlab[cell0[i]] : (u32)labels[i];
+      r = pix[i * 3];
+      g = pix[i * 3 + 1];
+      b = pix[i * 3 + 2];
+    }
+    const unsigned peers = __match_any_sync(kFull, lab);
+    const u32 sr = __reduce_add_sync(peers, r), sg = __reduce_add_sync(peers, g), sb = __reduce_add_sync(peers, b);
+    if (lab != 0xffffffffu && lane == __ffs(peers) - 1) {
+      u64* o = out + (i64)lab * 4;
+      atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)sr);
+      atomicAdd(reinterpret_cast<unsigned long long*>(o + 1), (unsigned long long)sg);
+      atomicAdd(reinterpret_cast<unsigned long long*>(o + 2), (unsigned long long)sb);
+      atomicAdd(reinterpret_cast<unsigned long long*>(o + 3), (unsigned long long)__popc(peers));
+    }
+  }
+}
+
 // labels in original order: one coalesced pass (cell0 -> run root -> rank)
 __global__ void __launch_bounds__(kThreads) k_labels_runs(const u32* __restrict__ cell0, i64 n,
                                                           const u32* __restrict__ runroot,

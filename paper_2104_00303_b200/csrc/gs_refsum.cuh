@@ -50,13 +50,41 @@ struct RsCtl {
   u32 nbig;       // segments that go through the global sort
   u32 maxlen;     // longest segment (observability)
   u32 nsingle;    // single-source cells whose closed form was recomputed (not cached)
-  u32 pad2[2];
+  u32 ncta;       // segments of kGatherWarp < len <= kGatherMax points (their ids: the CTA work list)
+  u32 pad2;
+};
+
+// Index-ordered point lists of the cells (sorted runs only).  Every cell of
+// table 0 is a run of the spatial sort, whose original indices perm[start,
+// end) ascend (the sort is stable): that is its list.  A cell that moves as a
+// whole keeps its list; a mixed target's list is the merge of its sources'
+// lists, written to the arena behind perm -- so a mixed target is ordered by
+// ranking each source's points among the other sources (binary searches),
+// not by sorting all of its points again.  Lists: (offset << 32 | length)
+// into `arena` (perm first), 0 = none (big segments, arena full): those
+// cells' later merges fall back to the gather + sort of their runs.  The
+// spatial sort places the points of a run in no particular order, so a run's
+// own list is flagged raw (kListRaw in the length word) and is put in index
+// order when a merge first loads it; published lists are ordered.
+constexpr u32 kListRaw = 0x80000000u;
+
+struct RsLists {
+  bool on;
+  const u64* cur;     // per slot of the source table
+  u64* nxt;           // per slot of the target table
+  u32* shead;         // per target slot: head of its source list (kRsEmpty-terminated)
+  u32* snext;         // per source slot: next source of the same target
+  u32* segdone;       // per segment: folded by a merge kernel
+  u32* arena;         // perm, then published lists
+  u64 cap;            // arena entries
+  unsigned long long* top;   // next free arena entry
 };
 
 // Segments up to kGatherMax points (sorted runs) are gathered from their runs
 // by one CTA and ordered in shared memory; longer ones (and every segment of
 // an unsorted run) go through the global radix sort.
 constexpr u32 kGatherMax = 8192;
+constexpr u32 kGatherWarp = 256;   // gathered segments up to this size: one warp each
 
 // ------------------------------------------------------- closed form
 
@@ -217,29 +245,33 @@ __device__ __forceinline__ void rs_load_tile(const Src& src, i64 base, i64 n, u3
   }
 }
 
-// per-tile digit counts, digit-major: counts[d * nblk + tile]
+// per-tile digit counts, digit-major: counts[d * nblk + tile].  The grid is
+// fixed (blocks loop over tiles), so a pass the device does not need costs one
+// small launch.
 template <class Src>
 __global__ void __launch_bounds__(kRsThreads) k_rs_count(Src src, const RsCtl* ctl, int pass, u32* counts,
                                                          u32 nblk) {
   __shared__ u32 hist[256];
   if (!rs_pass_live(ctl, pass)) return;
   const i64 n = src.count();
-  hist[threadIdx.x] = 0;
-  __syncthreads();
-  const i64 base = (i64)blockIdx.x * kRsTile;
-  if (base < n) {
-    u32 k[kRsItems], v[kRsItems];
-    bool ok[kRsItems];
-    rs_load_tile(src, base, n, k, v, ok);
+  for (u32 tile = blockIdx.x; tile < nblk; tile += gridDim.x) {
+    hist[threadIdx.x] = 0;
+    __syncthreads();
+    const i64 base = (i64)tile * kRsTile;
+    if (base < n) {
+      u32 k[kRsItems], v[kRsItems];
+      bool ok[kRsItems];
+      rs_load_tile(src, base, n, k, v, ok);
 #pragma unroll
-    for (int it = 0; it < kRsItems; ++it) {
-      const u32 d = ok[it] ? (k[it] >> (8 * pass)) & 255u : 256u;
-      const unsigned peers = __match_any_sync(kFull, d);
-      if (d < 256u && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[d], (u32)__popc(peers));
+      for (int it = 0; it < kRsItems; ++it) {
+        const u32 d = ok[it] ? (k[it] >> (8 * pass)) & 255u : 256u;
+        const unsigned peers = __match_any_sync(kFull, d);
+        if (d < 256u && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[d], (u32)__popc(peers));
+      }
     }
+    __syncthreads();
+    counts[(size_t)threadIdx.x * nblk + tile] = hist[threadIdx.x];
   }
-  __syncthreads();
-  counts[(size_t)threadIdx.x * nblk + blockIdx.x] = hist[threadIdx.x];
 }
 
 // exclusive scan of a u32 array (three kernels: chunk sums, top, apply)
@@ -335,11 +367,14 @@ __global__ void __launch_bounds__(kRsThreads, 4) k_rs_scatter(Src src, const RsC
   __shared__ u32 gofs[256];      // global offset of (digit, tile)
   __shared__ u32 sk[kRsTile];
   __shared__ u32 sv[kRsTile];
+  __shared__ u32 ws[kRsWarps];
   if (!rs_pass_live(ctl, pass)) return;
   const i64 n = src.count();
-  const i64 t0 = (i64)blockIdx.x * kRsTile;
-  if (t0 >= n) return;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (u32 tile = blockIdx.x; tile < nblk; tile += gridDim.x) {
+  const i64 t0 = (i64)tile * kRsTile;
+  if (t0 >= n) break;
+  __syncthreads();   // the previous tile's shared arrays are done with
   for (int q = threadIdx.x; q < kRsWarps * 256; q += kRsThreads) (&base[0][0])[q] = 0;
   __syncthreads();
   u32 k[kRsItems], v[kRsItems];
@@ -366,7 +401,7 @@ __global__ void __launch_bounds__(kRsThreads, 4) k_rs_scatter(Src src, const RsC
       acc += c;
     }
     tot = acc;
-    gofs[d] = offs[(size_t)d * nblk + blockIdx.x];
+    gofs[d] = offs[(size_t)d * nblk + tile];
   }
   // exclusive scan of the tile's digit counts (256 threads = 256 digits)
   {
@@ -376,7 +411,6 @@ __global__ void __launch_bounds__(kRsThreads, 4) k_rs_scatter(Src src, const RsC
       const u32 y = __shfl_up_sync(kFull, inc, o);
       if (lane >= o) inc += y;
     }
-    __shared__ u32 ws[kRsWarps];
     if (lane == 31) ws[w] = inc;
     __syncthreads();
     u32 wb = 0;
@@ -407,6 +441,7 @@ __global__ void __launch_bounds__(kRsThreads, 4) k_rs_scatter(Src src, const RsC
     const u32 out = gofs[d] + (e - tdig[d]);
     okeys[out] = kk;
     ovals[out] = sv[e];
+  }
   }
 }
 
@@ -623,8 +658,8 @@ __global__ void __launch_bounds__(256) k_fold_delta(RsSorted so, const RsCtl* ct
 // binade (or is a tie), that one is added in fp64, and the next chunk
 // starts right after it.  Exactly the sequential fp64 sum, at ~1 warp scan
 // per 32 elements instead of 32 dependent additions.
-template <int D, class Val>
-__device__ __forceinline__ double warp_fold(double s, const u32* __restrict__ vals, u32 a, u32 b, const Val& V, int j) {
+template <int D, class Val, class VT = u32>
+__device__ __forceinline__ double warp_fold(double s, const VT* __restrict__ vals, u32 a, u32 b, const Val& V, int j) {
   const int lane = threadIdx.x & 31;
   u32 i = a;
   u32 have = 0xffffffffu;   // chunk start the prefetched values belong to
@@ -774,7 +809,8 @@ template <int D, class Tab>
 __global__ void __launch_bounds__(kThreads) k_rs_classify(GridParams g, Tab cur, Tab nxt, const Rec<D>* __restrict__ rec,
                                                           Ctrl* ctrl, int c, int t, const u32* nsrc, u32* mid,
                                                           u32* outslot, double* rs_next, RsCtl* rsc, u32* seglen,
-                                                          u32* sstart, u32* send, bool all_big, Rec<D>* tag) {
+                                                          u32* sstart, u32* send, bool all_big, Rec<D>* tag,
+                                                          RsLists L, u32* ctalist) {
   if (block_stopped_before(ctrl, t)) return;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -802,18 +838,27 @@ __global__ void __launch_bounds__(kThreads) k_rs_classify(GridParams g, Tab cur,
         tag[ts] = tg;
         ++nrecomp;
       }
-    } else if (atomicCAS(mid + ts, kRsEmpty, kRsPending) == kRsEmpty) {
+      if (L.on) L.nxt[ts] = L.cur[s];   // the cell's index-ordered point list moves with it
+    } else {
+      if (L.on) L.snext[s] = atomicExch(L.shead + ts, s);   // source list of the mixed target
+      if (atomicCAS(mid + ts, kRsEmpty, kRsPending) != kRsEmpty) continue;
       const u32 m = atomicAdd(&rsc->nseg, 1u);
       const u32 len = (u32)nxt.ent[ts].count;
       outslot[m] = ts;
       seglen[m] = len;
       sstart[m] = 0;
       send[m] = 0;
+      if (L.on) {
+        L.nxt[ts] = 0;       // no list unless a merge publishes one
+        L.segdone[m] = 0;
+      }
       tag[ts].key = 0;   // the fold writes this slot: no cached closed form
       atomicMax(&rsc->maxlen, len);
       if (all_big || len > kGatherMax) {
         atomicAdd(&rsc->nelem, len);
         atomicAdd(&rsc->nbig, 1u);
+      } else if (len > kGatherWarp) {
+        ctalist[atomicAdd(&rsc->ncta, 1u)] = m;
       }
       mid[ts] = m;
     }
@@ -859,7 +904,6 @@ __global__ void __launch_bounds__(kThreads) k_rs_fill(const u32* runs, const u32
   }
 }
 
-constexpr u32 kGatherWarp = 256;   // gathered segments up to this size: one warp each
 constexpr size_t kGatherWarpSmem = (size_t)8 * 2 * kGatherWarp * sizeof(u32);
 
 // One warp per gathered segment of <= kGatherWarp points (the common case
@@ -870,7 +914,7 @@ template <int D, class Val, bool kFirst>
 __global__ void __launch_bounds__(256) k_rs_gather_warp(const RsCtl* ctl, const u32* seglen, const u32* segbeg,
                                                         const u32* seglist, const u32* start, const u32* end,
                                                         const u32* perm, const u32* runval, Val V,
-                                                        const u32* outslot, double* rs, bool all_big) {
+                                                        const u32* outslot, double* rs, bool all_big, RsLists L) {
   extern __shared__ u32 wsm[];
   if (all_big) return;
   const u32 nseg = ctl->nseg;
@@ -882,6 +926,7 @@ __global__ void __launch_bounds__(256) k_rs_gather_warp(const RsCtl* ctl, const 
   for (i64 q = gw; q < nseg; q += nw) {
     const u32 len = seglen[q];
     if (len == 0 || len > kGatherWarp) continue;   // warp-uniform
+    if (!kFirst && L.on && L.segdone[q]) continue;   // folded by a list merge
     const u32 b0 = segbeg ? segbeg[q] : (u32)q;
     const u32 nr = segbeg ? segbeg[q + 1] - b0 : 1u;
     // runs: lane k copies run k, k+32, ... at its exclusive offset
@@ -933,6 +978,15 @@ __global__ void __launch_bounds__(256) k_rs_gather_warp(const RsCtl* ctl, const 
         }
         __syncwarp();
       }
+    if (!kFirst && L.on) {   // the sorted indices are the target's list
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(L.top, (unsigned long long)len);
+      at = __shfl_sync(kFull, at, 0);
+      if (at + len <= L.cap) {
+        for (u32 e = lane; e < len; e += 32) L.arena[at + e] = xi[e];
+        if (lane == 0) L.nxt[outslot[q]] = (at << 32) | len;
+      }
+    }
 #pragma unroll 1
     for (int j = 0; j < D; ++j) {
       const bool neg = V.get(xv[0], j) < 0.0;
@@ -953,18 +1007,22 @@ template <int D, class Val, bool kFirst>
 __global__ void __launch_bounds__(256) k_rs_gather(const RsCtl* ctl, const u32* seglen, const u32* segbeg,
                                                    const u32* seglist, const u32* start,
                                                    const u32* end, const u32* perm, const u32* runval, Val V,
-                                                   const u32* outslot, double* rs, bool all_big) {
+                                                   const u32* outslot, double* rs, bool all_big, RsLists L,
+                                                   const u32* ctalist) {
   extern __shared__ u32 gsm[];
   u32* sidx = gsm;
   u32* sval = gsm + kGatherMax;
   u32* roff = gsm + 2 * kGatherMax;
   __shared__ u32 wsum[8];
+  __shared__ unsigned long long pub_at;
   if (all_big) return;
-  const u32 nseg = ctl->nseg;
+  const u32 nwork = ctalist ? ctl->ncta : ctl->nseg;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (u32 q = blockIdx.x; q < nseg; q += gridDim.x) {
+  for (u32 wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+    const u32 q = ctalist ? ctalist[wi] : wi;
     const u32 len = seglen[q];
     if (len <= kGatherWarp || len > kGatherMax) continue;   // block-uniform
+    if (!kFirst && L.on && L.segdone[q]) continue;          // folded by a list merge
     const u32 b0 = segbeg ? segbeg[q] : q;
     const u32 nr = segbeg ? segbeg[q + 1] - b0 : 1u;
     // exclusive offsets of the segment's runs (block scan of their lengths)
@@ -1030,12 +1088,277 @@ __global__ void __launch_bounds__(256) k_rs_gather(const RsCtl* ctl, const u32* 
         }
         __syncthreads();
       }
+    if (!kFirst && L.on) {   // the sorted indices are the target's list
+      if (tid == 0) pub_at = atomicAdd(L.top, (unsigned long long)len);
+      __syncthreads();
+      const unsigned long long at = pub_at;
+      if (at + len <= L.cap) {
+        for (u32 e = tid; e < len; e += 256) L.arena[at + e] = sidx[e];
+        if (tid == 0) L.nxt[outslot[q]] = (at << 32) | len;
+      }
+    }
     if (w < D) {
       const bool neg = V.get(sval[0], w) < 0.0;
       const double sm = warp_fold<D>(0.0, sval, 0, len, V, w);
       if (lane == 0) rs[(i64)outslot[q] * D + w] = (neg && sm != 0.0) ? -sm : sm;
     }
     __syncthreads();
+  }
+}
+
+// ------------------------------------------------------- list merges
+
+// values of a merge: the sources' target coordinates, staged in shared memory
+struct LocVal {
+  const double* t;   // [source][D]
+  int d;
+  __device__ __forceinline__ double get(u32 k, int j) const { return t[k * d + j]; }
+};
+
+// number of entries of the ascending list a[0, n) below x
+__device__ __forceinline__ u32 list_rank(const u32* a, u32 n, u32 x) {
+  if (n == 0 || x < a[0]) return 0;
+  if (x > a[n - 1]) return n;
+  u32 lo = 0, hi = n;
+  while (lo < hi) {
+    const u32 m = (lo + hi) >> 1;
+    if (a[m] < x) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+constexpr u32 kMergeWarpSrc = 32;    // sources a warp merge handles
+constexpr size_t merge_warp_smem(int d) {
+  // per warp: in (256 u32), out (256 u32), source number (256 u8), offsets (33 u32), values (32 x d f64)
+  return (size_t)8 * (2 * kGatherWarp * 4 + kGatherWarp + 36 * 4 + kMergeWarpSrc * d * 8);
+}
+
+// One warp per mixed segment of <= kGatherWarp points whose sources all carry
+// lists: rank-merge, publish the merged list, fold in index order.
+template <int D>
+__global__ void __launch_bounds__(256) k_rs_merge_warp(const RsCtl* ctl, const u32* seglen, const u32* outslot,
+                                                       const Rec<D>* __restrict__ rec, RsLists L, double* rs) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  const u32 nseg = ctl->nseg;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr size_t per = 2 * kGatherWarp * 4 + kGatherWarp + 36 * 4 + kMergeWarpSrc * D * 8;
+  unsigned char* base = msm + (size_t)w * per;
+  double* tv = reinterpret_cast<double*>(base);                       // 32 x D
+  u32* xin = reinterpret_cast<u32*>(base + kMergeWarpSrc * D * 8);     // 256
+  u32* xout = xin + kGatherWarp;                                       // 256
+  u32* soff = xout + kGatherWarp;                                      // 33 (+3 pad)
+  unsigned char* xk = reinterpret_cast<unsigned char*>(soff + 36);     // 256
+  const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 q = gw; q < nseg; q += nw) {
+    const u32 len = seglen[q];
+    if (len == 0 || len > kGatherWarp) continue;   // warp-uniform
+    const u32 ts = outslot[q];
+    // the sources: lane k takes the k-th of the chain
+    u32 mysrc = kRsEmpty, m = 0;
+    {
+      u32 s = L.shead[ts];
+      while (s != kRsEmpty && m < kMergeWarpSrc) {
+        if ((u32)lane == m) mysrc = s;
+        s = L.snext[s];
+        ++m;
+      }
+      if (s != kRsEmpty) continue;                 // more sources than lanes: the gather path
+    }
+    const u64 lst = (u32)lane < m ? L.cur[mysrc] : 0ull;
+    const u32 mylen = (u32)lst & ~kListRaw, myoff = (u32)(lst >> 32);
+    const bool myraw = ((u32)lst & kListRaw) != 0;
+    if (__any_sync(kFull, (u32)lane < m && mylen == 0)) continue;   // a source without a list
+
+    u32 inc = mylen;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (__shfl_sync(kFull, inc, 31) != len) continue;               // (never) inconsistent lists
+    soff[lane] = inc - mylen;
+    if (lane == 31) soff[32] = inc;
+    if ((u32)lane < m) {
+      const Rec<D> r = rec[mysrc];
+#pragma unroll
+      for (int j = 0; j < D; ++j) tv[lane * D + j] = r.t[j];
+    }
+    __syncwarp();
+    for (u32 k = 0; k < m; ++k) {
+      const u32 o = __shfl_sync(kFull, myoff, k), l = __shfl_sync(kFull, mylen, k), so = soff[k];
+      for (u32 e = lane; e < l; e += 32) xin[so + e] = L.arena[o + e];
+    }
+    __syncwarp();
+    // raw lists (runs of the spatial sort): index order by counting ranks
+    const unsigned rawmask = __ballot_sync(kFull, myraw && (u32)lane < m);
+    for (unsigned rm = rawmask; rm; rm &= rm - 1) {
+      const u32 k = (u32)__ffs(rm) - 1, so = soff[k], l = soff[k + 1] - so;
+      if (l < 2) continue;
+      for (u32 e = lane; e < l; e += 32) {
+        const u32 x = xin[so + e];
+        u32 r = 0;
+        for (u32 f = 0; f < l; ++f) r += xin[so + f] < x;
+        xout[so + r] = x;
+      }
+      __syncwarp();
+      for (u32 e = lane; e < l; e += 32) xin[so + e] = xout[so + e];
+      __syncwarp();
+    }
+    for (u32 e = lane; e < len; e += 32) {
+      u32 k = 0;
+      while (soff[k + 1] <= e) ++k;
+      const u32 x = xin[e];
+      u32 r = e - soff[k];
+      for (u32 kk = 0; kk < m; ++kk)
+        if (kk != k) r += list_rank(xin + soff[kk], soff[kk + 1] - soff[kk], x);
+      xout[r] = x;
+      xk[r] = (unsigned char)k;
+    }
+    __syncwarp();
+    // publish the merged list
+    unsigned long long at = 0;
+    if (lane == 0) at = atomicAdd(L.top, (unsigned long long)len);
+    at = __shfl_sync(kFull, at, 0);
+    if (at + len <= L.cap) {
+      for (u32 e = lane; e < len; e += 32) L.arena[at + e] = xout[e];
+      if (lane == 0) L.nxt[ts] = (at << 32) | len;
+    }
+    const LocVal V{tv, D};
+#pragma unroll 1
+    for (int j = 0; j < D; ++j) {
+      const bool neg = tv[xk[0] * D + j] < 0.0;
+      const double sm = warp_fold<D>(0.0, xk, 0, len, V, j);
+      if (lane == 0) rs[(i64)ts * D + j] = (neg && sm != 0.0) ? -sm : sm;
+    }
+    if (lane == 0) L.segdone[q] = 1;
+    __syncwarp();
+  }
+}
+
+constexpr u32 kMergeSrc = 255;   // sources a CTA merge handles (source numbers are bytes)
+constexpr u32 kMergeRankSort = 96;   // raw lists up to this length: counting ranks (one warp)
+constexpr size_t merge_smem(int d) {
+  // in, out (kGatherMax u32 each), source number (kGatherMax u8), per source: offset, slot, list (u32, u32, u64), values
+  return (size_t)kGatherMax * 9 + 256 * 16 + 8 + (size_t)256 * d * 8;
+}
+
+// One CTA per mixed segment of kGatherWarp < len <= kGatherMax points.
+template <int D>
+__global__ void __launch_bounds__(256) k_rs_merge(const RsCtl* ctl, const u32* seglen, const u32* outslot,
+                                                  const Rec<D>* __restrict__ rec, RsLists L, double* rs,
+                                                  const u32* ctalist) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  double* tv = reinterpret_cast<double*>(msm);                          // 256 x D
+  u64* slst = reinterpret_cast<u64*>(msm + (size_t)256 * D * 8);        // 256
+  u32* soff = reinterpret_cast<u32*>(slst + 256);                       // 257 (+1 pad)
+  u32* ssrc = soff + 258;                                               // 256
+  u32* xin = ssrc + 256;                                                // kGatherMax
+  u32* xout = xin + kGatherMax;                                         // kGatherMax
+  unsigned char* xk = reinterpret_cast<unsigned char*>(xout + kGatherMax);   // kGatherMax
+  __shared__ u32 sm_m, sm_ok;
+  __shared__ unsigned long long sm_at;
+  const u32 nwork = ctl->ncta;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (u32 wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+    const u32 q = ctalist[wi];
+    const u32 len = seglen[q];
+    const u32 ts = outslot[q];
+    __syncthreads();
+    if (tid == 0) {
+      u32 s = L.shead[ts], m = 0, tot = 0, ok = 1;
+      while (s != kRsEmpty && m < kMergeSrc) {
+        const u64 lst = L.cur[s];
+        ssrc[m] = s;
+        slst[m] = lst;
+        soff[m] = tot;
+        tot += (u32)lst & ~kListRaw;
+        ok &= ((u32)lst & ~kListRaw) != 0;
+        s = L.snext[s];
+        ++m;
+      }
+      soff[m] = tot;
+      sm_m = m;
+      sm_ok = ok && s == kRsEmpty && tot == len;
+    }
+    __syncthreads();
+    if (!sm_ok) continue;
+    const u32 m = sm_m;
+    for (u32 e = tid; e < m * D; e += 256) tv[e] = rec[ssrc[e / D]].t[e % D];
+    for (u32 k = w; k < m; k += 8) {
+      const u64 lst = slst[k];
+      const u32 o = (u32)(lst >> 32), l = (u32)lst & ~kListRaw, so = soff[k];
+      for (u32 e = lane; e < l; e += 32) xin[so + e] = L.arena[o + e];
+    }
+    __syncthreads();
+    // raw lists (runs of the spatial sort) are put in index order first: long
+    // ones by a block-wide bitonic sort in the output buffer, short ones by
+    // counting ranks, a warp each
+    for (u32 k = 0; k < m; ++k) {
+      const u32 so = soff[k], l = soff[k + 1] - so;
+      if (!((u32)slst[k] & kListRaw) || l <= kMergeRankSort) continue;   // block-uniform
+      u32 P = 1;
+      while (P < l) P <<= 1;
+      for (u32 e = tid; e < P; e += 256) xout[e] = e < l ? xin[so + e] : 0xffffffffu;
+      __syncthreads();
+      for (u32 kk = 2; kk <= P; kk <<= 1)
+        for (u32 jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (u32 e = tid; e < P; e += 256) {
+            const u32 x = e ^ jj;
+            if (x > e) {
+              const u32 a = xout[e], b = xout[x];
+              if ((a > b) == ((e & kk) == 0)) {
+                xout[e] = b;
+                xout[x] = a;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      for (u32 e = tid; e < l; e += 256) xin[so + e] = xout[e];
+      __syncthreads();
+    }
+    for (u32 k = w; k < m; k += 8) {
+      const u32 so = soff[k], l = soff[k + 1] - so;
+      if (!((u32)slst[k] & kListRaw) || l > kMergeRankSort || l < 2) continue;
+      for (u32 e = lane; e < l; e += 32) {
+        const u32 x = xin[so + e];
+        u32 r = 0;
+        for (u32 f = 0; f < l; ++f) r += xin[so + f] < x;
+        xout[so + r] = x;
+      }
+      __syncwarp();
+      for (u32 e = lane; e < l; e += 32) xin[so + e] = xout[so + e];
+    }
+    __syncthreads();
+    for (u32 e = tid; e < len; e += 256) {
+      // rank of point e (of source k) among the points of the other sources
+      u32 k = 0, hi = m;
+      while (hi - k > 1) {
+        const u32 md = (k + hi) >> 1;
+        if (soff[md] <= e) k = md; else hi = md;
+      }
+      const u32 x = xin[e];
+      u32 r = e - soff[k];
+      for (u32 kk = 0; kk < m; ++kk)
+        if (kk != k) r += list_rank(xin + soff[kk], soff[kk + 1] - soff[kk], x);
+      xout[r] = x;
+      xk[r] = (unsigned char)k;
+    }
+    if (tid == 0) sm_at = atomicAdd(L.top, (unsigned long long)len);
+    __syncthreads();
+    const unsigned long long at = sm_at;
+    if (at + len <= L.cap) {
+      for (u32 e = tid; e < len; e += 256) L.arena[at + e] = xout[e];
+      if (tid == 0) L.nxt[ts] = (at << 32) | len;
+    }
+    if (w < D) {
+      const LocVal V{tv, D};
+      const bool neg = tv[xk[0] * D + w] < 0.0;
+      const double sm = warp_fold<D>(0.0, xk, 0, len, V, w);
+      if (lane == 0) rs[(i64)ts * D + w] = (neg && sm != 0.0) ? -sm : sm;
+    }
+    if (tid == 0) L.segdone[q] = 1;
   }
 }
 
@@ -1131,7 +1454,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_first(GridParams g, Tab tab, co
                                                        bool sorted, bool gather, LowBits lb, u32* rc0, u32* runkey,
                                                        u32* outslot, double* rs, RsCtl* rsc, u32* seglen,
                                                        u32* sstart, u32* send, u32* seglist, u64* runkv,
-                                                       const int* lowrun) {
+                                                       const int* lowrun, u64* lst0) {
   const u32 nr = *nruns;
   const int lane = threadIdx.x & 31;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -1163,6 +1486,8 @@ __global__ void __launch_bounds__(kThreads) k_rs_first(GridParams g, Tab tab, co
         exact &= ok;
       }
       rc0[r] = slot;
+      // the run's indices: perm[start, start + len), in placement order
+      if (lst0) lst0[slot] = len < kListRaw ? (((u64)start[r] << 32) | len | kListRaw) : 0ull;
     }
     const bool seg = valid && !exact;
     const bool big = seg && (!gather || len > kGatherMax);
@@ -1231,9 +1556,14 @@ __global__ void k_rs_stats(const RsCtl* rsc, u32* out) {
 }
 
 // reset the mixed marks of the targets just folded
-__global__ void k_rs_unmark(const u32* outslot, const RsCtl* rsc, u32* mid) {
+__global__ void k_rs_unmark(const u32* outslot, const RsCtl* rsc, u32* mid, u32* shead) {
   const u32 ns = rsc->nseg;
-  for (u32 q = blockIdx.x * blockDim.x + threadIdx.x; q < ns; q += gridDim.x * blockDim.x) mid[outslot[q]] = kRsEmpty;
+  for (u32 q = blockIdx.x * blockDim.x + threadIdx.x; q < ns; q += gridDim.x * blockDim.x) {
+    mid[outslot[q]] = kRsEmpty;
+    if (shead) shead[outslot[q]] = kRsEmpty;
+  }
 }
+
+__global__ void k_rs_set64(unsigned long long* p, unsigned long long v) { *p = v; }
 
 }  // namespace gs

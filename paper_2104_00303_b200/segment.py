@@ -102,11 +102,18 @@ def segment_image(img: Image, cfg: ShiftConfig, mode: str = "rgb", engine: str =
     if engine not in ENGINES:
         raise ValueError(f"engine must be one of {sorted(ENGINES)}, got {engine!r}")
     labeling, trace = segment_pixels(img, cfg, mode, scale)
-    return segment_map_from_labeling(img, labeling), trace
+    # SegmentMap on device (segment.py:109-117): the labels come back in
+    # raster order; the per-segment colour sums were accumulated on the GPU
+    # next to the label delivery (gs_fetch_mean_colors), exact in integers
+    mean = np.empty((labeling.k, 3), dtype=np.float64)
+    _lib.check(_lib.load().gs_fetch_mean_colors(_lib.context(), _lib.ptr(mean), labeling.k))
+    return SegmentMap(labels=labeling.labels.reshape(img.height, img.width), k=labeling.k,
+                      mean_colors=mean), trace
 
 
 def segment_map_from_labeling(img: Image, labeling: Labeling) -> SegmentMap:
-    """segment.py:109-117 (host fold of the labels onto the raster)."""
+    """segment.py:109-117 on the host, for labelings that did not come from
+    segment_image (which gets the mean colours from the device)."""
     labels = labeling.labels.reshape(img.height, img.width)
     rgb = img.pixels.reshape(-1, 3).astype(np.float64)
     k = labeling.k

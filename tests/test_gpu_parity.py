@@ -290,6 +290,24 @@ def test_segment_fused_features_match_host_features():
     assert np.array_equal(lab.labels, r["labels"])
 
 
+@pytest.mark.parametrize("shape,mode", [((96, 64), "rgbxy"), ((96, 64), "rgb"), ((640, 360), "rgb"),
+                                        ((640, 360), "rgbxy")])
+def test_segment_map_mean_colours_on_device(shape, mode):
+    """SegmentMap from segment_image (mean colours accumulated on the GPU,
+    gs_fetch_mean_colors) equals segment_map_from_labeling on the host --
+    the reference's np.bincount fold (segment.py:109-117) -- bit for bit, for
+    small (per-point labels on device) and sorted (per-cell label delivery)
+    images, dense and hash tables."""
+    img = gs.Image(W.voronoi_image(shape[0], shape[1], 12, seed=5))
+    cfg = gs.ShiftConfig(h=10.0, eta=1e-3, max_iters=30)
+    seg, _ = gs.segment_image(img, cfg, mode=mode, scale=0.25)
+    lab = gs.Labeling(labels=seg.labels.ravel(), k=seg.k, modes=np.zeros((seg.k, 3)))
+    host = gs.segment_map_from_labeling(img, lab)
+    assert seg.mean_colors.shape == (seg.k, 3)
+    assert np.array_equal(seg.mean_colors.view(np.uint64), host.mean_colors.view(np.uint64))
+    assert np.array_equal(seg.labels, host.labels)
+
+
 # ------------------------------------------------------- full BASELINE sizes
 
 def test_cfg0_full_vs_reference():
