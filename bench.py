@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=100_000_000, help="points (cfg4 default 1e8)")
+    ap.add_argument("--workload", choices=["cfg4", "cfg2"], default="cfg4",
+                    help="cfg4 (default, the headline): the 100M-point cloud; cfg2: one 4K RGBxy image per GPU "
+                         "(weak scaling, no data-path collective)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-kernels", action="store_true", default=True)
@@ -460,6 +463,122 @@ def our_arm(a):
         print(json.dumps(line), flush=True)
 
 
+def cfg2_arm(a):
+    """cfg2 (BASELINE configs[2]): a batch of 3840x2160 RGB+xy images, one per
+    GPU (rank r segments image r; no collective on the data path,
+    cli.py:206-216).  `value`: features resident in HBM, the engine run only;
+    `e2e`: segment_image with uint8 host pixels (fused features, labels and
+    mean colours back on the host)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_00303_b200 as gs
+    from paper_2104_00303_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ["GRIDSHIFT_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = W.CONFIGS["cfg2"]
+    cfg = gs.ShiftConfig(c["h"], c["eta"], c["max_iters"])
+    img = gs.Image(W.cfg2_image(rank % 8))
+    x = gs.image_to_features(img, "rgbxy", 0.25).data
+    n, d = x.shape
+    x_dev = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    labels = torch.empty(n, dtype=torch.int64, device="cuda")
+
+    def step():
+        return gs.meanshiftpp_device(x_dev, cfg, labels)[2]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    _lib.profile(1)
+    iters_total = 0
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        w0 = time.time()
+        e0.record()
+        for _ in range(a.steps):
+            iters_total += step()
+        e1.record()
+        torch.cuda.synchronize()
+        clk.window(w0, time.time())
+        barrier()
+    ms = e0.elapsed_time(e1)
+    prof = _lib.profile(2)
+    _lib.profile(0)
+    # end to end: uint8 pixels from pinned host memory, labels + mean colours back
+    pix = torch.empty(img.pixels.shape, dtype=torch.uint8, pin_memory=True).numpy()
+    pix[:] = img.pixels
+    himg = gs.Image(pix)
+    gs.segment_image(himg, cfg, "rgbxy", scale=0.25)
+    esteps = min(a.steps, 5)
+    barrier()
+    t0 = time.perf_counter()
+    eit = 0
+    for _ in range(esteps):
+        seg, tr = gs.segment_image(himg, cfg, "rgbxy", scale=0.25)
+        eit += tr.iterations
+    esecs = time.perf_counter() - t0
+    import ctypes as C
+
+    hb, db = C.c_int64(0), C.c_int64(0)
+    _lib.check(_lib.load().gs_fetch_transfer_bytes(_lib.context(local), _lib.ref(hb), _lib.ref(db)))
+    tot_iters, e_ups = iters_total, n * eit
+    if world > 1:
+        t = torch.tensor([ms, esecs], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, esecs = float(t[0]), float(t[1])
+        u = torch.tensor([iters_total, n * eit], dtype=torch.float64, device="cuda")
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+        tot_iters, e_ups = float(u[0]), float(u[1])
+    peak, peak_src = measured_peak()
+    kernels = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
+    roofs = {}
+    for kind, per_launch in (("hist", 8 * d * n), ("shift", 16 * d * n)):
+        if prof[kind][1] and prof[kind][0] > 0:
+            ach = per_launch * prof[kind][1] / (prof[kind][0] / 1e3) / 1e9
+            roofs[kind] = {"kernel": "k_hist" if kind == "hist" else "k_shift", "bound": "hbm", "achieved": ach,
+                           "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                           "peak_source": peak_src, "alg_bytes_per_launch": per_launch,
+                           "avg_launch_ms": prof[kind][0] / prof[kind][1],
+                           "bytes_note": ("8*d*n B read per launch" if kind == "hist" else
+                                          "16*d*n B per launch (read y, write y'; SURVEY 8d)")}
+    line = {"metric": METRIC, "value": n * tot_iters / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": max(3, a.warmup), "ms_per_step": ms / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Voronoi image, paper_2104_00303_b200/workloads.py)",
+            "config": {"workload": f"cfg2: one 3840x2160 RGB+xy image per GPU (n={n:,} fp64 points, d=5, "
+                                   f"h={c['h']}, tol={c['eta']}, max_iter={c['max_iters']}, scale=0.25), "
+                                   "sparse 5-D lattice (hash tables)",
+                       "n_per_gpu": n, "d": d, "h": c["h"], "tol": c["eta"], "max_iter": c["max_iters"],
+                       "sharding": "one image per rank, no data-path collective",
+                       "l2": "the iterate (2 x 332 MB fp64) exceeds the 126 MB L2"},
+            "iterations_per_step": iters_total / a.steps, "roofline": roofs.get("shift"),
+            "roofline_hist": roofs.get("hist"), "kernels": kernels,
+            "gpu_launches": int(sum(v[1] for v in prof.values())), "clocks": clk.summary(),
+            "e2e": {"value": e_ups / esecs, "unit": UNIT, "h2d_bytes_per_step": int(hb.value),
+                    "d2h_bytes_per_step": int(db.value), "steps": esteps,
+                    "api": "paper_2104_00303_b200.segment_image(Image uint8 (2160, 3840, 3), ShiftConfig, "
+                           "'rgbxy', scale=0.25) -> gs_segment_image (C ABI)"}}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def refsum_stats(gs, iters):
     """Per-table counters of the reference-order sums in the last timed run."""
     st = gs.modeseek.last_refsum_stats(iters)
@@ -589,6 +708,8 @@ def main():
     a = parse()
     if a.impl == "reference":
         reference_arm(a)
+    elif a.workload == "cfg2":
+        cfg2_arm(a)
     else:
         our_arm(a)
 

@@ -20,7 +20,7 @@ LIB_PATH = Path(os.environ.get("GRIDSHIFT_LIB", Path(__file__).resolve().parent 
 GS_OK, GS_EINVAL, GS_ERUNTIME, GS_EUNSUPPORTED = 0, 1, 2, 3
 GS_DTYPE_F64, GS_DTYPE_F32 = 0, 1
 GS_OPT_COLLAPSED = 1
-GS_OPT_SUMS, GS_SUMS_REFERENCE, GS_SUMS_EXACT = 2, 0, 1
+GS_OPT_SUMS, GS_SUMS_REFERENCE, GS_SUMS_EXACT, GS_SUMS_SEQMODEL = 2, 0, 1, 2
 
 _P = C.c_void_p
 _i32 = C.c_int32

@@ -79,6 +79,7 @@ struct Prof {
 // into the context's buffers, sized by rs_alloc.
 struct RsRun {
   bool on = false;
+  bool model = false;    // GS_SUMS_SEQMODEL: closed forms + proportional folds, no point order
   int64_t n = 0;
   u32 nblk = 0;          // radix tiles over n points
   int maxpasses = 0;     // radix passes that can be needed for the segment ids
@@ -165,7 +166,8 @@ struct gs_ctx {
   int64_t xfer_h2d = 0, xfer_d2h = 0;   // last host call (gs_fetch_transfer_bytes)
   size_t slotlab_bytes = 0;
   // reference-order sums (gs_refsum.cuh): option + buffers
-  bool exact_sums = false;              // GS_OPT_SUMS
+  bool exact_sums = false;              // GS_OPT_SUMS: GS_SUMS_EXACT
+  bool seq_model = true;                // GS_OPT_SUMS: GS_SUMS_SEQMODEL, the default (sequential sums without the point order)
   // the last per-point run's iterate (gs_fetch_iterate)
   int64_t it_n = 0;
   int it_d = 0;
@@ -438,9 +440,11 @@ struct SortInfo {
 // offsets are 32-bit; a full arena only costs speed)
 inline u64 arena_entries(int64_t n) { return std::min<u64>(4ull * (u64)n, 0xfffffff0ull); }
 
-RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 segcap, int max_iters = 1) {
+RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 segcap, int max_iters = 1,
+                bool model = false) {
   RsRun& R = c->rsr;
   R.on = true;
+  R.model = model;
   R.n = n;
   R.slots = p.slots;
   R.segcap = std::max<u64>(segcap, 1);
@@ -450,8 +454,8 @@ RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 se
   for (int b = 0; b < 2; ++b) {
     R.rs[b] = ensure<double>(c, c->rsb[b], (size_t)p.slots * d);
     R.rc[b] = ensure<u32>(c, c->rs_rc[b], runs_cap);
-    R.k[b] = ensure<u32>(c, c->rs_k[b], (size_t)n);
-    R.v[b] = ensure<u32>(c, c->rs_v[b], (size_t)n);
+    R.k[b] = model ? nullptr : ensure<u32>(c, c->rs_k[b], (size_t)n);
+    R.v[b] = model ? nullptr : ensure<u32>(c, c->rs_v[b], (size_t)n);
   }
   R.nsrc = ensure<u32>(c, c->rs_nsrc, p.slots);
   R.mid = ensure<u32>(c, c->rs_mid, p.slots);
@@ -462,7 +466,7 @@ RsRun& rs_alloc(gs_ctx* c, const Plan& p, int d, int64_t n, u64 runs_cap, u64 se
   R.runval = ensure<u32>(c, c->rs_rval, runs_cap);
   R.cnt = ensure<u32>(c, c->rs_cnt, 256ull * R.nblk);
   R.scan = ensure<u32>(c, c->rs_scan, (256ull * R.nblk + kScan32Chunk - 1) / kScan32Chunk + 1);
-  const size_t nw = (size_t)(n / kFoldWin) + 1;
+  const size_t nw = model ? 1 : (size_t)(n / kFoldWin) + 1;
   R.wsum = ensure<double>(c, c->rs_wsum, nw * d);
   R.wpre = ensure<double>(c, c->rs_wpre, nw * d);
   R.wdelta = ensure<u64>(c, c->rs_wdelta, nw * d);
@@ -567,9 +571,11 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
       launch(c, K_REFSUM, [&] { k_rs_set64<<<1, 1, 0, c->st>>>(R.arena_top, (unsigned long long)n); });
     }
   } else {
-    u32* c0 = ensure<u32>(c, c->rs_cell0, (size_t)n);
-    launch(c, K_REFSUM, [&] { k_rs_cell0<D, Tab><<<blocks_for(c, n), kThreads, 0, c->st>>>(ys, n, p.g, tabs[0], c0); });
-    R.cell0 = c0;
+    if (!R.model) {
+      u32* c0 = ensure<u32>(c, c->rs_cell0, (size_t)n);
+      launch(c, K_REFSUM, [&] { k_rs_cell0<D, Tab><<<blocks_for(c, n), kThreads, 0, c->st>>>(ys, n, p.g, tabs[0], c0); });
+      R.cell0 = c0;
+    }
     if constexpr (Tab::kDense) {
       u32* rl = ensure<u32>(c, c->rs_runs, p.list_cap);
       GS_CUDA(cudaMemsetAsync(&ctrl->nruns, 0, sizeof(u32), c->st));
@@ -596,7 +602,7 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
     coarse_ok &= lb.v[j] >= -p.g.qexp[j] && lb.v[j] >= (e - 1) - 52;
   }
   int* lowrun = nullptr;
-  if (si && !coarse_ok) {
+  if (si && !coarse_ok && !R.model) {
     // per-run lowest bits over the sorted iterate (one pass)
     lowrun = reinterpret_cast<int*>(ensure<u32>(c, c->rs_lowrun, (size_t)p.slots * D));
     GS_CUDA(cudaMemsetAsync(lowrun, 0x7f, sizeof(int) * p.slots * D, c->st));   // large positive
@@ -607,8 +613,12 @@ void rs_first(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, const SortInfo* si
     k_rs_first<D, Tab><<<blocks_for(c, (int64_t)p.list_cap), kThreads, 0, c->st>>>(
         p.g, tabs[0], R.runs, R.nruns, si ? si->start : nullptr, ys, si != nullptr, !R.all_big, lb, R.rc[0],
         R.runkey, R.outslot, R.rs[0], R.ctl, R.seglen, R.sstart, R.send, R.seglist, R.runkv, lowrun,
-        R.arena_cap ? R.lst[0] : nullptr);
+        R.arena_cap ? R.lst[0] : nullptr, R.model);
   });
+  if (R.model) {   // the first table's sums: exact (distinct values; no order to model)
+    check_launch();
+    return;
+  }
   if (!R.all_big) {
     static std::atomic<uint64_t> wattr{0};
     if (attr_pending(wattr, c->device)) {
@@ -645,18 +655,38 @@ void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int cur = t & 1;
   GS_CUDA(cudaMemsetAsync(R.ctl, 0, sizeof(RsCtl), c->st));
-  GS_CUDA(cudaMemsetAsync(R.segbeg, 0, sizeof(u32) * (R.segcap + 1), c->st));
-  GS_CUDA(cudaMemsetAsync(R.segcur, 0, sizeof(u32) * R.segcap, c->st));
+  if (!R.model) {
+    GS_CUDA(cudaMemsetAsync(R.segbeg, 0, sizeof(u32) * (R.segcap + 1), c->st));
+    GS_CUDA(cudaMemsetAsync(R.segcur, 0, sizeof(u32) * R.segcap, c->st));
+  }
   const int64_t items = Tab::kDense ? (int64_t)p.slots : (int64_t)p.list_cap;
-  const RsLists L{R.arena_cap != 0, R.lst[cur], R.lst[cur ^ 1], R.shead, R.snext, R.segdone,
+  const bool lists = R.arena_cap != 0 && !R.model;
+  const RsLists L{lists || R.model, lists, R.lst[cur], R.lst[cur ^ 1], R.shead, R.snext, R.segdone,
                   const_cast<u32*>(R.perm), R.arena_cap, R.arena_top};
+  if (R.model) {
+    // sequential model: closed forms in k_rs_classify, proportional folds of
+    // the mixed targets' sources -- no point order, no sorts
+    launch(c, K_REFSUM, [&] {
+      k_rs_classify<D, Tab><<<blocks_for(c, items), kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur, t,
+                                                                          R.nsrc, R.mid, R.outslot, R.rs[cur ^ 1], R.ctl,
+                                                                          R.seglen, R.sstart, R.send, false,
+                                                                          static_cast<Rec<D>*>(R.tag[cur ^ 1]), L, nullptr);
+    });
+    launch(c, K_REFSUM, [&] {
+      k_rs_runfold<D, Tab><<<c->sms * 16, kModelWarps * 32, 0, c->st>>>(R.ctl, R.outslot, tabs[cur], rec, L, R.rs[cur ^ 1]);
+    });
+    if (t + 1 < R.stats_rows) launch(c, K_REFSUM, [&] { k_rs_stats<<<1, 1, 0, c->st>>>(R.ctl, R.stats + 5 * (t + 1)); });
+    launch(c, K_REFSUM, [&] { k_rs_unmark<<<blocks_for(c, (int64_t)R.segcap), kThreads, 0, c->st>>>(R.outslot, R.ctl, R.mid, R.shead); });
+    GS_CUDA(cudaMemsetAsync(R.nsrc, 0, sizeof(u32) * p.slots, c->st));
+    return;
+  }
   launch(c, K_REFSUM, [&] {
     k_rs_classify<D, Tab><<<blocks_for(c, items), kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur, t,
                                                                         R.nsrc, R.mid, R.outslot, R.rs[cur ^ 1], R.ctl,
                                                                         R.seglen, R.sstart, R.send, R.all_big,
                                                                         static_cast<Rec<D>*>(R.tag[cur ^ 1]), L, R.ctalist);
   });
-  if (L.on) {
+  if (L.lists) {
     // mixed targets whose sources carry point lists: rank-merge + fold
     static std::atomic<uint64_t> mattr{0};
     if (attr_pending(mattr, c->device)) {
@@ -1169,7 +1199,7 @@ bool spatial_sort(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, SortInfo& si, 
   si.cell0 = ensure<u32>(c, c->cell0, (size_t)n);
   si.slots0 = p.slots;
   // reference-order sums: perm, followed by the arena of merged point lists
-  si.perm = c->exact_sums ? nullptr : ensure<u32>(c, c->perm, (size_t)arena_entries(n));
+  si.perm = (c->exact_sums || c->seq_model) ? nullptr : ensure<u32>(c, c->perm, (size_t)arena_entries(n));
   si.runroot = off;   // the cursors are dead once the scatter is done...
   si.end = off;       // ...except as run ends, read (collapsed mode) before runroot is written
   GS_CUDA(cudaMemsetAsync(si.minidx, 0xff, p.slots * sizeof(u32), c->st));
@@ -1305,7 +1335,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   // reference-order sums (default): the first table's sums in np.bincount
   // order, from the input values in original point order
   if (!c->exact_sums) {
-    rs_alloc(c, p, D, n, sorted ? sinfo.slots0 : p.slots, p.list_cap, max_iters);
+    rs_alloc(c, p, D, n, sorted ? sinfo.slots0 : p.slots, p.list_cap, max_iters, c->seq_model);
     InVal<D> V{nullptr, 2, soa_ld(n)};
     if (sorted && aos_in && p.dense)
       V = InVal<D>{in.dev, in.kind == IN_F32 ? 1 : 0, 0};
@@ -1465,7 +1495,7 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   reset_ctrl(c);
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   // reference-order sums: the step equals the reference's bit for bit
-  const bool rs = !c->exact_sums;
+  const bool rs = !c->exact_sums;   // (distinct input values: the sequential model is the reference's order too)
   if (rs) rs_alloc(c, p, D, n, p.slots, p.list_cap);
   const InVal<D> V{y0, 2, soa_ld(n)};
   if (p.dense) {
@@ -1557,7 +1587,7 @@ int64_t run_tables_d(gs_ctx* c, const double* xdev, int64_t n, double h, int64_t
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const int nb_pts = blocks_for(c, n);
   // reference-order sums (default): the reference's tables bit for bit
-  const bool rs = !c->exact_sums;
+  const bool rs = !c->exact_sums;   // (distinct input values: the sequential model is the reference's order too)
   if (rs) rs_alloc(c, p, D, n, p.slots, p.list_cap);
   const InVal<D> V{y0, 2, soa_ld(n)};
   if (p.dense) {
@@ -1927,8 +1957,11 @@ int gs_ctx_set_option(gs_ctx* c, int32_t option, int64_t value) {
   return guarded(c, [&] {
     if (option == GS_OPT_COLLAPSED)
       c->collapsed = value != 0;
-    else if (option == GS_OPT_SUMS && (value == GS_SUMS_REFERENCE || value == GS_SUMS_EXACT))
+    else if (option == GS_OPT_SUMS && (value == GS_SUMS_REFERENCE || value == GS_SUMS_EXACT || value == GS_SUMS_SEQMODEL))
+    {
       c->exact_sums = value == GS_SUMS_EXACT;
+      c->seq_model = value == GS_SUMS_SEQMODEL;
+    }
     else
       fail(GS_EINVAL, "unknown option or value");
   });

@@ -69,7 +69,8 @@ struct RsCtl {
 constexpr u32 kListRaw = 0x80000000u;
 
 struct RsLists {
-  bool on;
+  bool on;            // source chains of the mixed targets (shead / snext)
+  bool lists;         // cells carry point lists (cur / nxt / arena)
   const u64* cur;     // per slot of the source table
   u64* nxt;           // per slot of the target table
   u32* shead;         // per target slot: head of its source list (kRsEmpty-terminated)
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_classify(GridParams g, Tab cur,
         tag[ts] = tg;
         ++nrecomp;
       }
-      if (L.on) L.nxt[ts] = L.cur[s];   // the cell's index-ordered point list moves with it
+      if (L.lists) L.nxt[ts] = L.cur[s];   // the cell's index-ordered point list moves with it
     } else {
       if (L.on) L.snext[s] = atomicExch(L.shead + ts, s);   // source list of the mixed target
       if (atomicCAS(mid + ts, kRsEmpty, kRsPending) != kRsEmpty) continue;
@@ -848,7 +849,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_classify(GridParams g, Tab cur,
       seglen[m] = len;
       sstart[m] = 0;
       send[m] = 0;
-      if (L.on) {
+      if (L.lists) {
         L.nxt[ts] = 0;       // no list unless a merge publishes one
         L.segdone[m] = 0;
       }
@@ -857,7 +858,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_classify(GridParams g, Tab cur,
       if (all_big || len > kGatherMax) {
         atomicAdd(&rsc->nelem, len);
         atomicAdd(&rsc->nbig, 1u);
-      } else if (len > kGatherWarp) {
+      } else if (ctalist && len > kGatherWarp) {
         ctalist[atomicAdd(&rsc->ncta, 1u)] = m;
       }
       mid[ts] = m;
@@ -926,7 +927,7 @@ __global__ void __launch_bounds__(256) k_rs_gather_warp(const RsCtl* ctl, const 
   for (i64 q = gw; q < nseg; q += nw) {
     const u32 len = seglen[q];
     if (len == 0 || len > kGatherWarp) continue;   // warp-uniform
-    if (!kFirst && L.on && L.segdone[q]) continue;   // folded by a list merge
+    if (!kFirst && L.lists && L.segdone[q]) continue;   // folded by a list merge
     const u32 b0 = segbeg ? segbeg[q] : (u32)q;
     const u32 nr = segbeg ? segbeg[q + 1] - b0 : 1u;
     // runs: lane k copies run k, k+32, ... at its exclusive offset
@@ -978,7 +979,7 @@ __global__ void __launch_bounds__(256) k_rs_gather_warp(const RsCtl* ctl, const 
         }
         __syncwarp();
       }
-    if (!kFirst && L.on) {   // the sorted indices are the target's list
+    if (!kFirst && L.lists) {   // the sorted indices are the target's list
       unsigned long long at = 0;
       if (lane == 0) at = atomicAdd(L.top, (unsigned long long)len);
       at = __shfl_sync(kFull, at, 0);
@@ -1022,7 +1023,7 @@ __global__ void __launch_bounds__(256) k_rs_gather(const RsCtl* ctl, const u32* 
     const u32 q = ctalist ? ctalist[wi] : wi;
     const u32 len = seglen[q];
     if (len <= kGatherWarp || len > kGatherMax) continue;   // block-uniform
-    if (!kFirst && L.on && L.segdone[q]) continue;          // folded by a list merge
+    if (!kFirst && L.lists && L.segdone[q]) continue;          // folded by a list merge
     const u32 b0 = segbeg ? segbeg[q] : q;
     const u32 nr = segbeg ? segbeg[q + 1] - b0 : 1u;
     // exclusive offsets of the segment's runs (block scan of their lengths)
@@ -1088,7 +1089,7 @@ __global__ void __launch_bounds__(256) k_rs_gather(const RsCtl* ctl, const u32* 
         }
         __syncthreads();
       }
-    if (!kFirst && L.on) {   // the sorted indices are the target's list
+    if (!kFirst && L.lists) {   // the sorted indices are the target's list
       if (tid == 0) pub_at = atomicAdd(L.top, (unsigned long long)len);
       __syncthreads();
       const unsigned long long at = pub_at;
@@ -1362,6 +1363,208 @@ __global__ void __launch_bounds__(256) k_rs_merge(const RsCtl* ctl, const u32* s
   }
 }
 
+// ------------------------------------------------------- sequential model
+// GS_SUMS_SEQMODEL: the reference's sequential per-cell sums without the
+// point order.  A single-source cell is c copies of one value: the closed
+// form, bit for bit.  A mixed target holds c_a copies of each source value
+// v_a, interleaved in index order in the reference.  While the accumulator
+// stays inside one binade every addition of v_a adds the same number of ulps
+// whatever came before (ties aside), so the sum depends on the order only
+// through WHICH additions happen before each binade crossing.  The model
+// takes a well-mixed order: inside a binade the remaining copies of every
+// source are consumed in proportion (one integer multiply-add per source),
+// up to the crossing, which is made by single fp64 additions in ascending
+// slot order; then the next binade.  Deterministic, a function of the cell
+// table only (so independent of how points are split across GPUs), and
+// O(sources x binades) per cell instead of O(points).
+constexpr u32 kModelSrc = 256;       // sources per target handled in shared memory (3^5 = 243)
+constexpr int kModelWarps = 4;
+
+__device__ __forceinline__ u64 warp_sum_u64(u64 x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  return x;
+}
+__device__ __forceinline__ double warp_sum_f64(double x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  return x;
+}
+
+// One warp folds `m` sources (counts cnt[], magnitudes val[], ascending slot
+// order) into the magnitude of their modelled sequential sum.  rem / inc are
+// the warp's scratch (m entries each).
+__device__ __forceinline__ double model_fold(u32 m, const u32* cnt, const double* val, u32* rem, u64* inc) {
+  const int lane = threadIdx.x & 31;
+  for (u32 a = lane; a < m; a += 32) rem[a] = cnt[a];
+  __syncwarp();
+  double s = 0.0;
+  for (;;) {
+    u64 left = 0;
+    for (u32 a = lane; a < m; a += 32) left += rem[a];
+    left = warp_sum_u64(left);
+    if (left == 0) break;
+    bool single = false;          // make single additions this round (first addition / subnormal)
+    int be = 0;
+    if (s == 0.0) {
+      single = true;
+    } else {
+      const u64 sb = dbits(s);
+      be = (int)(sb >> 52);
+      if (be <= 1) {
+        single = true;
+      } else {
+        const int ue = be - 1075;
+        u64 mi = (sb & ((1ull << 52) - 1)) | (1ull << 52);
+        const u64 room = kMaxM - mi;
+        double totd = 0.0;
+        for (u32 a = lane; a < m; a += 32) {
+          u64 ia = 0;
+          if (rem[a]) {
+            const double x = scale2(val[a], -ue);
+            if (x >= 0x1p53) {
+              ia = 1ull << 53;                       // crosses at once
+            } else {
+              const double fl = floor(x);
+              const double fr = x - fl;
+              ia = (u64)fl + ((fr > 0.5 || (fr == 0.5 && ((u64)fl & 1ull))) ? 1ull : 0ull);
+            }
+            totd += (double)rem[a] * (double)ia;
+          }
+          inc[a] = ia;
+        }
+        totd = warp_sum_f64(totd);
+        if (totd == 0.0) break;                       // further additions change nothing
+        if (totd <= (double)room * (1.0 - 0x1p-20)) {
+          // everything left fits this binade: order-free
+          u64 t = 0;
+          for (u32 a = lane; a < m; a += 32) t += (u64)rem[a] * inc[a];
+          mi += warp_sum_u64(t);
+          s = scale2((double)mi, ue);
+          break;
+        }
+        // proportional share of every source up to the crossing
+        const double f = (double)room / totd * (1.0 - 0x1p-30);
+        u64 tk = 0;
+        for (u32 a = lane; a < m; a += 32) {
+          u32 take = 0;
+          if (rem[a] && inc[a] < (1ull << 53)) {
+            const double w = floor(f * (double)rem[a]);
+            take = w <= 0.0 ? 0u : (w >= (double)rem[a] ? rem[a] : (u32)w);
+          }
+          tk += (u64)take * inc[a];
+          rem[a] -= take;
+          inc[a] = take;                              // (the step is used up; keep the share for an undo)
+        }
+        tk = warp_sum_u64(tk);
+        if (tk > room) {                              // (numerical safety) undo the shares
+          for (u32 a = lane; a < m; a += 32) rem[a] += (u32)inc[a];
+          tk = 0;
+        }
+        mi += tk;
+        s = scale2((double)mi, ue);
+        __syncwarp();
+        single = true;                                // the crossing: single additions
+      }
+    }
+    if (single) {
+      // single fp64 additions in ascending slot order until the binade changes
+      // (one pass at most; the outer loop re-plans)
+      __syncwarp();
+      for (u32 a = 0; a < m; ++a) {
+        if (rem[a] == 0) continue;                    // warp-uniform (shared memory)
+        const bool first = s == 0.0;
+        s = first ? val[a] : dadd(s, val[a]);
+        __syncwarp();
+        if (lane == 0) rem[a] -= 1;
+        __syncwarp();
+        if (first || (int)(dbits(s) >> 52) != be) break;
+      }
+    }
+    __syncwarp();
+  }
+  return s;
+}
+
+template <int D, class Tab>
+__global__ void __launch_bounds__(kModelWarps * 32) k_rs_runfold(const RsCtl* ctl, const u32* outslot, Tab cur,
+                                                                 const Rec<D>* __restrict__ rec, RsLists L,
+                                                                 double* rs) {
+  __shared__ u32 s_slot[kModelWarps][kModelSrc];
+  __shared__ u32 s_cnt[kModelWarps][kModelSrc];
+  __shared__ u32 s_rem[kModelWarps][kModelSrc];
+  __shared__ double s_val[kModelWarps][kModelSrc];
+  __shared__ u64 s_inc[kModelWarps][kModelSrc];
+  const u32 nseg = ctl->nseg;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  u32* sl = s_slot[w];
+  const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 q = gw; q < nseg; q += nw) {
+    const u32 ts = outslot[q];
+    // the sources, ascending by slot (the chain's order is first-come)
+    u32 m = 0;
+    for (u32 s = L.shead[ts]; s != kRsEmpty; s = L.snext[s]) {
+      if (m < kModelSrc && lane == 0) sl[m] = s;
+      ++m;
+    }
+    if (m > kModelSrc) {
+      // more sources than the buffers hold (d >= 6 only): source by source,
+      // ascending slots found by repeated walks of the chain
+      if (lane < D) {
+        double acc = 0.0;
+        bool neg = false;
+        i64 last = -1;
+        for (u32 a = 0; a < m; ++a) {
+          u32 best = kRsEmpty;
+          for (u32 s = L.shead[ts]; s != kRsEmpty; s = L.snext[s])
+            if ((i64)s > last && s < best) best = s;
+          last = (i64)best;
+          const double v = rec[best].t[lane];
+          neg |= v < 0.0;
+          acc = seqsum_mag_from(acc, fabs(v), cur.ent[best].count);
+        }
+        rs[(i64)ts * D + lane] = (neg && acc != 0.0) ? -acc : acc;
+      }
+      __syncwarp();
+      continue;
+    }
+    u32 P = 1;
+    while (P < m) P <<= 1;
+    for (u32 e = m + lane; e < P; e += 32) sl[e] = kRsEmpty;
+    __syncwarp();
+    for (u32 k = 2; k <= P; k <<= 1)
+      for (u32 jj = k >> 1; jj > 0; jj >>= 1) {
+        for (u32 e = lane; e < P; e += 32) {
+          const u32 x = e ^ jj;
+          if (x > e) {
+            const u32 a = sl[e], b = sl[x];
+            if ((a > b) == ((e & k) == 0)) {
+              sl[e] = b;
+              sl[x] = a;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    for (u32 a = lane; a < m; a += 32) s_cnt[w][a] = (u32)cur.ent[sl[a]].count;
+#pragma unroll 1
+    for (int j = 0; j < D; ++j) {
+      bool neg = false;
+      for (u32 a = lane; a < m; a += 32) {
+        const double v = rec[sl[a]].t[j];
+        neg |= v < 0.0;
+        s_val[w][a] = fabs(v);
+      }
+      neg = __any_sync(kFull, neg);
+      __syncwarp();
+      const double acc = model_fold(m, s_cnt[w], s_val[w], s_rem[w], s_inc[w]);
+      if (lane == 0) rs[(i64)ts * D + j] = (neg && acc != 0.0) ? -acc : acc;
+      __syncwarp();
+    }
+  }
+}
+
 // Per run of the sorted first iterate: the lowest set bit over its values
 // (per axis; atomicMin into low[slot * D + j], initialised to 4096).  A warp
 // walks 4096 consecutive positions, 32 at a time, carrying the open run's
@@ -1454,7 +1657,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_first(GridParams g, Tab tab, co
                                                        bool sorted, bool gather, LowBits lb, u32* rc0, u32* runkey,
                                                        u32* outslot, double* rs, RsCtl* rsc, u32* seglen,
                                                        u32* sstart, u32* send, u32* seglist, u64* runkv,
-                                                       const int* lowrun, u64* lst0) {
+                                                       const int* lowrun, u64* lst0, bool force_exact) {
   const u32 nr = *nruns;
   const int lane = threadIdx.x & 31;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -1483,7 +1686,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_first(GridParams g, Tab tab, co
         bool ok = lbj >= -g.qexp[j];
         const double up = fabs(S[j]) * (1.0 + 0x1p-50);
         if (up > 0.0) ok &= lbj >= (int)(dbits(up) >> 52) - 1023 - 52;
-        exact &= ok;
+        exact &= ok || force_exact;
       }
       rc0[r] = slot;
       // the run's indices: perm[start, start + len), in placement order

@@ -47,3 +47,14 @@ def exact_sums():
 
     with gs.sum_order("exact"):
         yield
+
+
+@pytest.fixture
+def reference_sums():
+    """Run the engine with reference-order sums (GS_SUMS_REFERENCE): every
+    iterate equals the reference's bit for bit -- the tests that assert
+    bitwise trajectories."""
+    import paper_2104_00303_b200 as gs
+
+    with gs.sum_order("reference"):
+        yield
