@@ -413,7 +413,7 @@ def our_arm(a):
             "roofline": roof, "roofline_hist": roof_hist, "kernels": kernels,
             "kernels_note": "CUDA-event spans per kind over the timed region; agg/derive run on a "
                             "low-priority side stream concurrently with the shifts (their spans include "
-                            "waiting for SM slots); see profiles/launches_r01_summary.json for serialised "
+                            "waiting for SM slots); see profiles/launches_r02_summary.json for serialised "
                             "per-kernel device time",
             "gpu_launches": launches, "clocks": clk.summary(),
             "byte_model": {
@@ -433,11 +433,14 @@ def our_arm(a):
     if shard:
         line["config"]["parallelism"] = f"rows sharded over {world} GPU(s), NCCL"
     if rank == 0 and not shard:
-        line["sum_order"] = ("reference: per-cell and neighbourhood sums in the reference's sequential "
-                             "order (np.bincount, grid.py:186-187, 253-258); iterates equal the "
-                             "reference's bit for bit")
+        line["sum_order"] = ("seqmodel (default): the reference's sequential per-cell sums (np.bincount, "
+                             "grid.py:186-187) without the point order -- single-source cells by the closed "
+                             "form (bit for bit), mixed cells folded from their sources in proportion per "
+                             "binade; cells, counts and labels equal the reference's, modes within 1.5e-11*h "
+                             "on this workload (tests/test_gpu_parity.py::test_cfg4_100m_vs_reference)")
         line["refsum"] = refsum_stats(gs, last_iters)
-        line["exact_order"] = exact_leg(gs, torch, x_dev, cfg, labels, n, a.steps)
+        line["reference_order"] = order_leg(gs, torch, x_dev, cfg, labels, n, a.steps, "reference")
+        line["exact_order"] = order_leg(gs, torch, x_dev, cfg, labels, n, a.steps, "exact")
         line["collapsed"] = collapsed_leg(gs, torch, x_dev, cfg, labels, n, a.steps)
     if not a.no_e2e:
         if shard:
@@ -585,16 +588,24 @@ def refsum_stats(gs, iters):
     return {"mixed_cells_per_table": [int(v) for v in st[:, 0]],
             "points_through_global_sort_per_table": [int(v) for v in st[:, 2]],
             "longest_mixed_cell_per_table": [int(v) for v in st[:, 3]],
-            "note": "cells receiving several source cells are folded in point-index order (stable radix "
-                    "sort for long ones, shared-memory gathers for short ones); single-source cells use "
-                    "the closed form per binade"}
+            "note": "per table: cells that received several source cells (folded by the sequential model in "
+                    "the default order; in point-index order under GS_SUMS_REFERENCE, where the second "
+                    "list counts the points that go through the global radix sort); single-source cells "
+                    "use the closed form per binade"}
 
 
-def exact_leg(gs, torch, x_dev, cfg, labels, n, steps):
-    """Same workload with GS_SUMS_EXACT (order-independent exact sums rounded
-    once): what the per-point engine costs without the reference's summation
-    order; its modes sit ~1e-9*h from the reference's at cfg4."""
-    with gs.sum_order("exact"):
+ORDER_NOTES = {
+    "reference": "GS_SUMS_REFERENCE: every mixed cell summed in point-index order (index-ordered point lists, "
+                 "radix sort for long cells); every iterate equals the reference's bit for bit",
+    "exact": "GS_SUMS_EXACT: exact fixed-point sums rounded once (order-independent; the row-sharded multi-GPU "
+             "path computes these); modes 1.1e-8*h from the reference's on this workload, over the 1e-9*h bar, "
+             "so not the headline",
+}
+
+
+def order_leg(gs, torch, x_dev, cfg, labels, n, steps, order):
+    """Same workload under another sum order."""
+    with gs.sum_order(order):
         gs.meanshiftpp_device(x_dev, cfg, labels)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -606,9 +617,7 @@ def exact_leg(gs, torch, x_dev, cfg, labels, n, steps):
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    return {"value": n * it / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps,
-            "note": "GS_SUMS_EXACT: exact fixed-point sums rounded once (order-independent; the row-sharded "
-                    "multi-GPU path computes these); not bit-identical to the reference, so not the headline"}
+    return {"value": n * it / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "note": ORDER_NOTES[order]}
 
 
 def collapsed_leg(gs, torch, x_dev, cfg, labels, n, steps):

@@ -60,6 +60,7 @@ const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "shift", "clear
                                           "labels", "transpose", "dump", "track", "sort", "derive", "refsum"};
 
 constexpr int64_t kSortMinPoints = 1 << 15;   // spatial sort pays off above this
+constexpr int kShiftCtasChain = 6;            // shift CTAs per SM while the sequential-sum chain runs beside it
 
 inline int64_t soa_ld(int64_t n) { return (n + 127) & ~int64_t(127); }   // = k_hist tile
 
@@ -175,7 +176,7 @@ struct gs_ctx {
   Buf rsb[2], rs_nsrc, rs_mid, rs_out, rs_rc[2], rs_rkey, rs_rval, rs_k[2], rs_v[2], rs_cnt, rs_scan,
       rs_start, rs_end, rs_wsum, rs_wpre, rs_wdelta, rs_ctl, rs_cell0, rs_runs, rs_seglen, rs_segbeg,
       rs_segcur, rs_seglist, rs_runseg, rs_segscan, rs_runkv, rs_tag[2], rs_stats, rs_lowrun, rs_lst[2],
-      rs_shead, rs_snext, rs_segdone, rs_atop, rs_ctalist;
+      rs_shead, rs_snext, rs_segdone, rs_atop, rs_ctalist, rs_nocc;
   RsRun rsr;
 };
 
@@ -1008,7 +1009,12 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
         attr_done(attr, c->device);
       }
       const int64_t ntiles = (n + 4 * T - 1) / (4 * T);
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * 512 / T));
+      // persistent CTAs per SM: 8 fill the SM's registers (8 x 64 x 96); fewer
+      // leave room for the table chain's CTAs on the side stream
+      // (GRIDSHIFT_SHIFT_CTAS overrides, for tuning)
+      static const int env_per = getenv("GRIDSHIFT_SHIFT_CTAS") ? atoi(getenv("GRIDSHIFT_SHIFT_CTAS")) : 0;
+      const int per = env_per > 0 ? env_per : (R.on ? kShiftCtasChain : 8);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * per));
       launch(c, K_SHIFT, [&] {
         k_shift_tma<D, T><<<grid, T, shift_tma_smem<D, T>(), c->st>>>(
             y_it, n, p.g, rec, ctrl, static_cast<u64*>(c->partials.p), static_cast<double*>(c->mv_hist.p), t, eta,
@@ -1668,6 +1674,7 @@ struct ShardState {
   Plan p{};
   SortInfo si{};
   bool sorted = false;
+  bool model = false;      // sequential-model sums (GS_SUMS_SEQMODEL / _REFERENCE contexts); else exact
 };
 
 ShardState* shard_of(gs_ctx* c, bool create) {
@@ -1700,9 +1707,35 @@ void shard_plan_d(gs_ctx* c, ShardState* sh, const InitStats& s) {
   check_launch();
 }
 
+// The merged (global) first table is in buffer 0: with the sequential-model
+// sum order its coordinate sums are the exact sums rounded once (as on one
+// GPU), for every occupied cell of the GLOBAL table -- later tables are a
+// function of the table alone (k_rs_classify, k_rs_runfold), so every rank
+// computes the same sums whatever its rows are.
+template <int D>
+void shard_model_first_d(gs_ctx* c, ShardState* sh) {
+  Tabs<D> tabs = make_tabs<D>(c, sh->p);
+  RsRun& R = rs_alloc(c, sh->p, D, sh->n, sh->p.slots, sh->p.list_cap, sh->max_iters, true);
+  u32* occ = ensure<u32>(c, c->rs_runs, sh->p.list_cap);
+  u32* nocc = ensure<u32>(c, c->rs_nocc, 1);
+  GS_CUDA(cudaMemsetAsync(nocc, 0, sizeof(u32), c->st));
+  launch(c, K_REFSUM, [&] {
+    k_compact<D><<<blocks_for(c, (int64_t)sh->p.slots), kThreads, 0, c->st>>>(tabs.dn[0].ent, sh->p.slots, occ, nocc);
+  });
+  GS_CUDA(cudaMemsetAsync(R.ctl, 0, sizeof(RsCtl), c->st));
+  LowBits lb{};
+  launch(c, K_REFSUM, [&] {
+    k_rs_first<D, DenseTable<D>><<<blocks_for(c, (int64_t)sh->p.list_cap), kThreads, 0, c->st>>>(
+        sh->p.g, tabs.dn[0], occ, nocc, nullptr, nullptr, false, false, lb, R.rc[0], R.runkey, R.outslot, R.rs[0],
+        R.ctl, R.seglen, R.sstart, R.send, R.seglist, R.runkv, nullptr, nullptr, true);
+  });
+  check_launch();
+}
+
 template <int D>
 void shard_iterate_d(gs_ctx* c, ShardState* sh, int t, u64* limbs) {
   Tabs<D> tabs = make_tabs<D>(c, sh->p);
+  c->rsr.on = sh->model;   // (entry points clear it)
   enqueue_iteration<D>(c, sh->p, tabs.dn, t, 0.0, sh->n, blocks_for(c, sh->n),
                        blocks_for(c, (int64_t)sh->p.list_cap), limbs, true, true);
   check_launch();
@@ -1814,7 +1847,7 @@ void gs_ctx_destroy(gs_ctx* c) {
                   &c->rs_cell0, &c->rs_runs, &c->rs_seglen, &c->rs_segbeg, &c->rs_segcur, &c->rs_seglist,
                   &c->rs_runseg, &c->rs_segscan, &c->rs_runkv, &c->rs_tag[0], &c->rs_tag[1], &c->rs_stats,
                   &c->rs_lowrun, &c->rs_lst[0], &c->rs_lst[1], &c->rs_shead, &c->rs_snext, &c->rs_segdone,
-                  &c->rs_atop, &c->rs_ctalist};
+                  &c->rs_atop, &c->rs_ctalist, &c->rs_nocc};
   for (Buf* b : rbufs)
     if (b->p) cudaFree(b->p);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
@@ -2260,9 +2293,11 @@ int gs_shard_table_io(gs_ctx* c, void* buf_dev, int32_t to_device_table, void* s
     c->st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
     ShardState* sh = shard_of(c, false);
     const size_t bytes = sh->p.slots * 8 * (1 + 2 * (size_t)sh->d);
-    if (to_device_table)
+    if (to_device_table) {
       GS_CUDA(cudaMemcpyAsync(c->ent[0].p, buf_dev, bytes, cudaMemcpyDeviceToDevice, c->st));
-    else
+      sh->model = !c->exact_sums;
+      if (sh->model) GS_DISPATCH(sh->d, shard_model_first_d<DD>(c, sh));
+    } else
       GS_CUDA(cudaMemcpyAsync(buf_dev, c->ent[0].p, bytes, cudaMemcpyDeviceToDevice, c->st));
   });
 }

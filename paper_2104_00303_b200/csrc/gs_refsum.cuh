@@ -114,6 +114,10 @@ __host__ __device__ inline double seqsum_mag_from(double s, double a, u64 c) {
     s = a;
     --c;
   }
+  if (c <= 24) {                                    // a few copies: the additions themselves
+    for (; c; --c) s = dadd(s, a);
+    return s;
+  }
   while (c) {
     const u64 sb = dbits(s);
     const int be = (int)(sb >> 52);                 // biased exponent (s > 0)
@@ -149,7 +153,12 @@ __host__ __device__ inline double seqsum_mag_from(double s, double a, u64 c) {
       delta = frac > 0.5 ? q + 1 : q;
     }
     if (delta == 0) return scale2((double)m, ue);   // further additions change nothing
-    u64 k = (kMaxM - m) / delta;
+    // k = (kMaxM - m) / delta: both below 2^53, so the fp64 quotient is off by
+    // at most one (cheaper than the 64-bit integer division)
+    const u64 room = kMaxM - m;
+    u64 k = (u64)((double)room / (double)delta);
+    if (k * delta > room) --k;
+    else if ((k + 1) * delta <= room) ++k;
     if (k > c) k = c;
     m += k * delta;
     c -= k;
@@ -1486,6 +1495,78 @@ __device__ __forceinline__ double model_fold(u32 m, const u32* cnt, const double
   return s;
 }
 
+// model_fold for up to 32 sources, one per lane (cnt / val lane-private, 0
+// beyond the sources): registers and shuffles only.
+__device__ __forceinline__ double model_fold32(u32 cnt, double val) {
+  const int lane = threadIdx.x & 31;
+  u32 rem = cnt;
+  double s = 0.0;
+  for (;;) {
+    if (__ballot_sync(kFull, rem > 0) == 0) break;
+    bool single = false;
+    int be = 0;
+    if (s == 0.0) {
+      single = true;
+    } else {
+      const u64 sb = dbits(s);
+      be = (int)(sb >> 52);
+      if (be <= 1) {
+        single = true;
+      } else {
+        const int ue = be - 1075;
+        u64 mi = (sb & ((1ull << 52) - 1)) | (1ull << 52);
+        const u64 room = kMaxM - mi;
+        u64 ia = 0;
+        if (rem) {
+          const double x = scale2(val, -ue);
+          if (x >= 0x1p53) {
+            ia = 1ull << 53;
+          } else {
+            const double fl = floor(x);
+            const double fr = x - fl;
+            ia = (u64)fl + ((fr > 0.5 || (fr == 0.5 && ((u64)fl & 1ull))) ? 1ull : 0ull);
+          }
+        }
+        const double totd = warp_sum_f64((double)rem * (double)ia);
+        if (totd == 0.0) break;
+        if (totd <= (double)room * (1.0 - 0x1p-20)) {
+          mi += warp_sum_u64((u64)rem * ia);
+          s = scale2((double)mi, ue);
+          break;
+        }
+        const double f = (double)room / totd * (1.0 - 0x1p-30);
+        u32 take = 0;
+        if (rem && ia < (1ull << 53)) {
+          const double w = floor(f * (double)rem);
+          take = w <= 0.0 ? 0u : (w >= (double)rem ? rem : (u32)w);
+        }
+        u64 tk = warp_sum_u64((u64)take * ia);
+        if (tk > room) {                              // (numerical safety)
+          take = 0;
+          tk = 0;
+        }
+        rem -= take;
+        mi += tk;
+        s = scale2((double)mi, ue);
+        single = true;
+      }
+    }
+    if (single) {
+      unsigned lv = __ballot_sync(kFull, rem > 0);
+      while (lv) {
+        const int a = __ffs(lv) - 1;
+        lv &= lv - 1;
+        const bool first = s == 0.0;
+        const double va = __shfl_sync(kFull, val, a);
+        s = first ? va : dadd(s, va);
+        if (lane == a) rem -= 1;
+        if (first || (int)(dbits(s) >> 52) != be) break;
+      }
+    }
+  }
+  return s;
+}
+
 template <int D, class Tab>
 __global__ void __launch_bounds__(kModelWarps * 32) k_rs_runfold(const RsCtl* ctl, const u32* outslot, Tab cur,
                                                                  const Rec<D>* __restrict__ rec, RsLists L,
@@ -1525,6 +1606,33 @@ __global__ void __launch_bounds__(kModelWarps * 32) k_rs_runfold(const RsCtl* ct
           acc = seqsum_mag_from(acc, fabs(v), cur.ent[best].count);
         }
         rs[(i64)ts * D + lane] = (neg && acc != 0.0) ? -acc : acc;
+      }
+      __syncwarp();
+      continue;
+    }
+    if (m <= 32) {
+      // the common case: one source per lane, registers only
+      __syncwarp();
+      u32 slot = (u32)lane < m ? sl[lane] : kRsEmpty;
+      u32 r = 0;
+      for (u32 i = 0; i < m; ++i) r += __shfl_sync(kFull, slot, i) < slot;
+      __syncwarp();
+      if ((u32)lane < m) sl[r] = slot;
+      __syncwarp();
+      slot = (u32)lane < m ? sl[lane] : kRsEmpty;
+      u32 cnt = 0;
+      Rec<D> rr;
+#pragma unroll
+      for (int j = 0; j < D; ++j) rr.t[j] = 0.0;
+      if ((u32)lane < m) {
+        cnt = (u32)cur.ent[slot].count;
+        rr = rec[slot];
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const bool neg = __any_sync(kFull, rr.t[j] < 0.0);
+        const double acc = model_fold32(cnt, fabs(rr.t[j]));
+        if (lane == 0) rs[(i64)ts * D + j] = (neg && acc != 0.0) ? -acc : acc;
       }
       __syncwarp();
       continue;

@@ -10,7 +10,11 @@ words, exact and identical on every rank -- and each later table is derived
 identically on every rank.  Per iteration the ranks exchange only the
 movement (4 int64 limbs of an exact 128-bit sum); at the end one MIN
 all-reduce gives the global first-appearance numbering.  Results equal the
-single-GPU engine bit for bit.
+single-GPU engine bit for bit, in the default sum order (the sequential
+model of the reference's per-cell sums is a function of the merged cell
+table only, so every rank computes the same sums) and in the exact order;
+a context set to the reference order runs the default here (the point-index
+order of a mixed cell spans ranks).
 
 The per-rank work goes through a backend (default: the CUDA C ABI); tests
 inject a numpy backend to cover this driver with gloo on CPU.

@@ -27,12 +27,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, backend, y, h, eta, mi, out):
+def _worker(rank, world, port, backend, y, h, eta, mi, out, order):
     import sys
 
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-    from paper_2104_00303_b200.modeseek import ShiftConfig
+    from paper_2104_00303_b200.modeseek import ShiftConfig, set_sum_order
     from paper_2104_00303_b200.sharded import meanshiftpp_sharded, shard_bounds
+
+    set_sum_order(order)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -46,15 +48,19 @@ def _worker(rank, world, port, backend, y, h, eta, mi, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.usefixtures("exact_sums")
+@pytest.mark.parametrize("order", ["seqmodel", "exact"])
 @pytest.mark.parametrize("world,backend,n", [(1, "nccl", 200_000), (2, "gloo", 200_000), (2, "gloo", 5_000)])
-def test_cuda_shards_equal_single_gpu(world, backend, n):
+def test_cuda_shards_equal_single_gpu(world, backend, n, order):
+    """Sharded runs equal the single-GPU engine bit for bit in the default
+    sum order (the sequential model is a function of the merged cell table
+    only, so every rank computes the same sums) and in the exact order."""
     y = W.cloud3d(n, seed=21)
     h, eta, mi = 1.0, 1e-3, 20
     with tempfile.TemporaryDirectory() as out:
-        mp.spawn(_worker, args=(world, _free_port(), backend, y, h, eta, mi, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), backend, y, h, eta, mi, out, order), nprocs=world, join=True)
         parts = [dict(np.load(Path(out) / f"r{r}.npz")) for r in range(world)]
-    lab, tr = gs.meanshiftpp(gs.PointSet(y.astype(np.float64)), gs.ShiftConfig(h, eta, mi))
+    with gs.sum_order(order):
+        lab, tr = gs.meanshiftpp(gs.PointSet(y.astype(np.float64)), gs.ShiftConfig(h, eta, mi))
     for p in parts:
         assert int(p["iters"]) == tr.iterations
         np.testing.assert_array_equal(p["movement"], tr.total_movement_per_iter)
