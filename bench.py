@@ -549,13 +549,16 @@ def cfg2_arm(a):
     peak, peak_src = measured_peak()
     kernels = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
     roofs = {}
+    # live launches: one histogram per run; one shift per iteration (the loop
+    # enqueues chunks ahead, launches past the stop flag exit at once)
+    live = {"hist": a.steps, "shift": iters_total}
     for kind, per_launch in (("hist", 8 * d * n), ("shift", 16 * d * n)):
         if prof[kind][1] and prof[kind][0] > 0:
-            ach = per_launch * prof[kind][1] / (prof[kind][0] / 1e3) / 1e9
+            ach = per_launch * live[kind] / (prof[kind][0] / 1e3) / 1e9
             roofs[kind] = {"kernel": "k_hist" if kind == "hist" else "k_shift", "bound": "hbm", "achieved": ach,
                            "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
                            "peak_source": peak_src, "alg_bytes_per_launch": per_launch,
-                           "avg_launch_ms": prof[kind][0] / prof[kind][1],
+                           "avg_launch_ms": prof[kind][0] / live[kind],
                            "bytes_note": ("8*d*n B read per launch" if kind == "hist" else
                                           "16*d*n B per launch (read y, write y'; SURVEY 8d)")}
     line = {"metric": METRIC, "value": n * tot_iters / (ms / 1e3), "unit": UNIT, "n_gpus": world,

@@ -1383,10 +1383,12 @@ __global__ void __launch_bounds__(256) k_rs_merge(const RsCtl* ctl, const u32* s
 // takes a well-mixed order: inside a binade the remaining copies of every
 // source are consumed in proportion (one integer multiply-add per source),
 // up to the crossing, which is made by single fp64 additions in ascending
-// slot order; then the next binade.  Deterministic, a function of the cell
+// slot order; then the next binade.  (Targets of at most kModelDirect points
+// are simply added up, one copy of every source per round.)  Deterministic, a function of the cell
 // table only (so independent of how points are split across GPUs), and
 // O(sources x binades) per cell instead of O(points).
 constexpr u32 kModelSrc = 256;       // sources per target handled in shared memory (3^5 = 243)
+constexpr u32 kModelDirect = 96;     // targets up to this many points (<= 32 sources): plain additions
 constexpr int kModelWarps = 4;
 
 __device__ __forceinline__ u64 warp_sum_u64(u64 x) {
@@ -1501,6 +1503,21 @@ __device__ __forceinline__ double model_fold32(u32 cnt, double val) {
   const int lane = threadIdx.x & 31;
   u32 rem = cnt;
   double s = 0.0;
+  if (__reduce_add_sync(kFull, cnt > kModelDirect ? kModelDirect + 1 : cnt) <= kModelDirect) {
+    // a small target: the additions themselves, one copy of every source per
+    // round in ascending slot order
+    for (;;) {
+      unsigned lv = __ballot_sync(kFull, rem > 0);
+      if (lv == 0) return s;
+      while (lv) {
+        const int a = __ffs(lv) - 1;
+        lv &= lv - 1;
+        const double va = __shfl_sync(kFull, val, a);
+        s = s == 0.0 ? va : dadd(s, va);
+      }
+      rem -= rem > 0;
+    }
+  }
   for (;;) {
     if (__ballot_sync(kFull, rem > 0) == 0) break;
     bool single = false;
