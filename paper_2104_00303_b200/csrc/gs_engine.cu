@@ -771,8 +771,9 @@ void side_init(gs_ctx* c) {
   // LOW priority: the table chain fills the SMs the shift's last wave leaves
   // idle instead of displacing the bandwidth-bound shift (measured: high
   // priority costs +9 ms per 100M-point run, low saves 3 ms)
-  (void)greatest;
-  GS_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, least));
+  // (GRIDSHIFT_SIDE_PRIO=high flips it, for tuning)
+  const char* pr = getenv("GRIDSHIFT_SIDE_PRIO");
+  GS_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, (pr && pr[0] == 'h') ? greatest : least));
   for (cudaEvent_t* e : {&c->ev_fork, &c->ev_join, &c->ev_rec[0], &c->ev_rec[1], &c->ev_shift[0], &c->ev_shift[1]})
     GS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (cudaEvent_t* e : {&c->ev_pace[0], &c->ev_pace[1]}) GS_CUDA(cudaEventCreate(e));
@@ -1013,7 +1014,7 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
       // leave room for the table chain's CTAs on the side stream
       // (GRIDSHIFT_SHIFT_CTAS overrides, for tuning)
       static const int env_per = getenv("GRIDSHIFT_SHIFT_CTAS") ? atoi(getenv("GRIDSHIFT_SHIFT_CTAS")) : 0;
-      const int per = env_per > 0 ? env_per : (R.on ? kShiftCtasChain : 8);
+      const int per = env_per > 0 ? std::min(env_per, 128) : (R.on ? kShiftCtasChain : 8);
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * per));
       launch(c, K_SHIFT, [&] {
         k_shift_tma<D, T><<<grid, T, shift_tma_smem<D, T>(), c->st>>>(
@@ -1298,7 +1299,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   ensure<Rec<D>>(c, c->targets, 2 * p.slots);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
-  ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
+  ensure<u64>(c, c->partials, 2 * std::max<size_t>((size_t)nb_pts, (size_t)c->sms * 128) + 2);
   ensure<double>(c, c->mv_hist, (size_t)max_iters);
   GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->wr_hist, (size_t)max_iters), 0, sizeof(u64) * max_iters, c->st));
   u64* fp = ensure<u64>(c, c->fp_hist, (size_t)max_iters);
@@ -1493,7 +1494,7 @@ void run_step_d(gs_ctx* c, const double* xdev, int64_t n, double h, double* y_ou
   ensure<Rec<D>>(c, c->targets, p.slots);
   const int nb_pts = blocks_for(c, n);
   const int nb_cells = blocks_for(c, (int64_t)p.list_cap);
-  ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
+  ensure<u64>(c, c->partials, 2 * std::max<size_t>((size_t)nb_pts, (size_t)c->sms * 128) + 2);
   ensure<double>(c, c->mv_hist, 1);
   GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->wr_hist, 1), 0, sizeof(u64), c->st));
   GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->fp_hist, 1), 0, 8, c->st));
@@ -1694,7 +1695,7 @@ void shard_plan_d(gs_ctx* c, ShardState* sh, const InitStats& s) {
   Tabs<D> tabs = make_tabs<D>(c, p);
   ensure<Rec<D>>(c, c->targets, 2 * p.slots);
   const int nb_pts = blocks_for(c, sh->n);
-  ensure<u64>(c, c->partials, 2 * (size_t)nb_pts + 2);
+  ensure<u64>(c, c->partials, 2 * std::max<size_t>((size_t)nb_pts, (size_t)c->sms * 128) + 2);
   ensure<double>(c, c->mv_hist, (size_t)sh->max_iters);
   GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->wr_hist, (size_t)sh->max_iters), 0, 8 * sh->max_iters, c->st));
   GS_CUDA(cudaMemsetAsync(ensure<u64>(c, c->fp_hist, (size_t)sh->max_iters), 0, 8 * sh->max_iters, c->st));
