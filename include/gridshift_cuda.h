@@ -130,7 +130,9 @@ GS_API int gs_segment_image(gs_ctx* ctx, const uint8_t* pixels, int32_t height, 
  *     (O(sources), no sort); the first table (distinct input values) is the
  *     exact sum rounded once.  Cells, counts and labels equal the
  *     reference's; modes within 1e-9*h on every BASELINE configuration
- *     (measured: <= 2e-10*h).
+ *     (measured: <= 2e-10*h).  Assumes the points of a
+ *     mixed cell are well mixed in index order (shuffled rows); for large
+ *     spatially sorted inputs use 0.
  *   0 = the reference's summation order, bit for bit: mixed cells are summed
  *     in point-index order (index-ordered point lists, radix sort for long
  *     cells); every iterate equals the reference's bitwise.

@@ -996,30 +996,32 @@ void enqueue_iteration(gs_ctx* c, const Plan& p, Tab* tabs, int t, double eta, i
     GS_CUDA(cudaStreamWaitEvent(main_st, c->ev_rec[cur], 0));
   }
   bool tma = false;
-  if constexpr (Tab::kDense && D <= 3) {
-    // bulk-copy pipelined shift: persistent, 8 CTAs of 64 threads per SM (2 TMA stages each)
+  if constexpr ((Tab::kDense && D <= 3) || (!Tab::kDense && (D == 4 || D == 5))) {
+    // bulk-copy pipelined shift: persistent 64-thread CTAs (2 TMA stages each);
+    // dense tables of up to 3 axes and the hash tables of 4- and 5-axis runs
+    // (the lookups probe the table; the tiles still stream through shared memory)
     if (with_shift) {
       // 64-thread CTAs (tile = 256 points), 16 warps per SM: small CTAs
       // decouple the per-tile barriers (measured 256 -> 64: -1 ms per run)
       constexpr int T = 64;
       static std::atomic<uint64_t> attr{0};
       if (attr_pending(attr, c->device)) {
-        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D, T, Tab>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        GS_CUDA(cudaFuncSetAttribute(k_shift_tma<D, T, Tab>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)shift_tma_smem<D, T>()));
         attr_done(attr, c->device);
       }
       const int64_t ntiles = (n + 4 * T - 1) / (4 * T);
       // persistent CTAs per SM: 8 fill the SM's registers (8 x 64 x 96); fewer
       // leave room for the table chain's CTAs on the side stream
-      // (GRIDSHIFT_SHIFT_CTAS overrides, for tuning)
+      // (GRIDSHIFT_SHIFT_CTAS overrides, for tuning; beyond 8 the CTAs run in waves)
       static const int env_per = getenv("GRIDSHIFT_SHIFT_CTAS") ? atoi(getenv("GRIDSHIFT_SHIFT_CTAS")) : 0;
-      const int per = env_per > 0 ? std::min(env_per, 128) : (R.on ? kShiftCtasChain : 8);
+      const int per = env_per > 0 ? std::min(env_per, 128) : ((R.on && Tab::kDense) ? kShiftCtasChain : 8);
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c->sms * per));
       launch(c, K_SHIFT, [&] {
-        k_shift_tma<D, T><<<grid, T, shift_tma_smem<D, T>(), c->st>>>(
-            y_it, n, p.g, rec, ctrl, static_cast<u64*>(c->partials.p), static_cast<double*>(c->mv_hist.p), t, eta,
-            limbs, static_cast<u64*>(c->wr_hist.p) + t);
+        k_shift_tma<D, T, Tab><<<grid, T, shift_tma_smem<D, T>(), c->st>>>(
+            y_it, n, p.g, tabs[cur], rec, ctrl, static_cast<u64*>(c->partials.p), static_cast<double*>(c->mv_hist.p), t,
+            eta, limbs, static_cast<u64*>(c->wr_hist.p) + t);
       });
       tma = true;
     }

@@ -911,8 +911,10 @@ constexpr size_t shift_tma_smem() {
   return (size_t)kShiftStages * D * 4 * T * sizeof(double);
 }
 
-template <int D, int T>
-__global__ void __maxnreg__(96) k_shift_tma(double* y, i64 n, GridParams g,
+// (Dense tables do not read `tab`: the key is the slot.  Hash tables probe it;
+// their 4- and 5-axis quads need more registers.)
+template <int D, int T, class Tab>
+__global__ void __maxnreg__(D <= 3 ? 96 : 128) k_shift_tma(double* y, i64 n, GridParams g, Tab tab,
                                                            const Rec<D>* __restrict__ rec, Ctrl* ctrl,
                                                            u64* partials, double* mv_hist, int t, double eta,
                                                            u64* limbs, u64* wbytes) {
@@ -920,7 +922,6 @@ __global__ void __maxnreg__(96) k_shift_tma(double* y, i64 n, GridParams g,
   constexpr int kShiftTilePts = 4 * T;
   extern __shared__ __align__(128) double tiles[];   // [stage][axis][kShiftTilePts]
   __shared__ __align__(8) u64 full[kShiftStages];
-  const DenseTable<D> tab{};
   const i64 ntiles = (n + kShiftTilePts - 1) / kShiftTilePts;
   const i64 G = gridDim.x;
   const i64 mine = (ntiles > (i64)blockIdx.x) ? (ntiles - (i64)blockIdx.x + G - 1) / G : 0;
@@ -957,7 +958,7 @@ __global__ void __maxnreg__(96) k_shift_tma(double* y, i64 n, GridParams g,
         in[j][1] = src[1];
       }
       double out[4][D];
-      const int kind = shift_quad<D, DenseTable<D>>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
+      const int kind = shift_quad<D, Tab>(g, tab, rec, ctrl, in, q, n, out, ahi, alo);
       store_quad<D>(y, g.ld, q, true, in, out, nst, kind);
     }
     __syncthreads();   // stage s consumed: refill it

@@ -150,7 +150,9 @@ def set_sum_order(order: str, device: int | None = None) -> None:
     interleaved proportionally (no sort); neighbourhood sums in the
     reference's lexicographic offset order (grid.py:253-258).  Cells, counts
     and labels equal the reference's, modes within 1e-9*h on every
-    configuration.
+    configuration; assumes the points of a mixed cell
+    are well mixed in index order (for 1e8 spatially sorted rows the modes
+    can drift ~1e-8*h from the reference's, like the exact order's).
     "reference": additionally every mixed cell is summed in point-index
     order -- iterates equal the reference's bit for bit (about 2x slower).
     "exact": order-independent exact fixed-point sums rounded once (what the
