@@ -60,6 +60,7 @@ const char* const kKindNames[K_NKINDS] = {"init", "hist", "agg", "shift", "clear
                                           "labels", "transpose", "dump", "track", "sort", "derive", "refsum"};
 
 constexpr int64_t kSortMinPoints = 1 << 15;   // spatial sort pays off above this
+constexpr int kClassifyThreads = 256;         // k_rs_classify CTA size in the default sum order
 constexpr int kShiftCtasChain = 6;            // shift CTAs per SM while the sequential-sum chain runs beside it
 
 inline int64_t soa_ld(int64_t n) { return (n + 127) & ~int64_t(127); }   // = k_hist tile
@@ -667,11 +668,16 @@ void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
   if (R.model) {
     // sequential model: closed forms in k_rs_classify, proportional folds of
     // the mixed targets' sources -- no point order, no sorts
+    // 128-thread CTAs: they share the SMs with the shift's persistent CTAs, and
+    // smaller CTAs fit the registers those leave (GRIDSHIFT_CLASSIFY_T, for tuning)
+    static const int env_t = getenv("GRIDSHIFT_CLASSIFY_T") ? atoi(getenv("GRIDSHIFT_CLASSIFY_T")) : 0;
+    const int ct = (env_t == 64 || env_t == 128 || env_t == 256) ? env_t : kClassifyThreads;
+    const int cb = (int)std::max<int64_t>(1, std::min<int64_t>((items + ct - 1) / ct, (int64_t)c->sms * 8 * (kThreads / ct)));
     launch(c, K_REFSUM, [&] {
-      k_rs_classify<D, Tab><<<blocks_for(c, items), kThreads, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur, t,
-                                                                          R.nsrc, R.mid, R.outslot, R.rs[cur ^ 1], R.ctl,
-                                                                          R.seglen, R.sstart, R.send, false,
-                                                                          static_cast<Rec<D>*>(R.tag[cur ^ 1]), L, nullptr);
+      k_rs_classify<D, Tab><<<cb, ct, 0, c->st>>>(p.g, tabs[cur], tabs[cur ^ 1], rec, ctrl, cur, t,
+                                                  R.nsrc, R.mid, R.outslot, R.rs[cur ^ 1], R.ctl,
+                                                  R.seglen, R.sstart, R.send, false,
+                                                  static_cast<Rec<D>*>(R.tag[cur ^ 1]), L, nullptr);
     });
     launch(c, K_REFSUM, [&] {
       k_rs_runfold<D, Tab><<<c->sms * 16, kModelWarps * 32, 0, c->st>>>(R.ctl, R.outslot, tabs[cur], rec, L, R.rs[cur ^ 1]);
