@@ -177,6 +177,46 @@ def test_cfg0_trajectory_bitwise_vs_reference():
     assert np.array_equal(lab.labels, r["labels"])
 
 
+def _dense_runs():
+    return [c for c in G.cases("runs") if G.case("runs", c)["y"].shape[1] <= 3]
+
+
+@pytest.mark.parametrize("c", _dense_runs() + ["cfg0", "cloud300k",
+                               pytest.param("cfg1", marks=pytest.mark.slow),
+                               pytest.param("cloud2m", marks=pytest.mark.slow)])
+def test_run_bitwise_vs_sequential_model(c):
+    """The DEFAULT sum order against its independent CPU restatement
+    (tests/seq_model.py: exact first table, closed form for single-source
+    cells, model_fold32 for mixed cells, sequential neighbourhood sums): the
+    final iterate -- hence every iterate, every closed form and every model
+    fold on the device -- plus movement trace, per-iteration tables, labels
+    and modes, bit for bit."""
+    from tests import seq_model as S
+
+    if c == "cfg0":
+        cfgd = W.CONFIGS["cfg0"]
+        y0, h, eta, mi = W.blobs2d(), cfgd["h"], cfgd["eta"], cfgd["max_iters"]
+    elif c == "cfg1":       # 2M pixels, 100 iterations, sorted dense path
+        cfgd = W.CONFIGS["cfg1"]
+        y0 = gs.image_to_features(gs.Image(W.cfg1_image()), "rgb").data
+        h, eta, mi = cfgd["h"], cfgd["eta"], cfgd["max_iters"]
+    elif c in ("cloud300k", "cloud2m"):   # the cfg4 generator (big merging cells), 50 iterations
+        n = 300_000 if c == "cloud300k" else 2_000_000
+        y0, h, eta, mi = W.cloud3d(n, seed=4).astype(np.float64), 1.0, 1e-3, 50
+    else:
+        f = G.case("runs", c)
+        y0, h, eta, mi = f["y"], float(f["h"]), _eta(f), int(f["max_iters"])
+    lab, tr = gs.meanshiftpp(gs.PointSet(y0), gs.ShiftConfig(h=h, eta=eta, max_iters=mi))
+    y = gs.modeseek.last_iterate(*y0.shape)
+    r = S.meanshiftpp(y0, h, eta, mi)
+    assert tr.iterations == r["iterations"] and tr.converged == r["converged"]
+    assert [int(v) for v in tr.fingerprint_per_iter] == [int(v) for v in r["iter_fp"]]
+    assert np.array_equal(y, r["y"])
+    np.testing.assert_array_equal(tr.total_movement_per_iter, r["movement"])
+    assert np.array_equal(lab.labels, r["labels"])
+    assert np.array_equal(lab.modes, r["modes"])
+
+
 @pytest.mark.usefixtures("exact_sums")
 @pytest.mark.parametrize("c", G.cases("runs"))
 def test_run_bitwise_vs_exact_model(c):

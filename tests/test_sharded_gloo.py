@@ -1,5 +1,5 @@
-"""Row-sharded driver (paper_2104_00303_b200/sharded.py) at world size 2 on
-CPU (gloo), with the numpy shard backend: the sharded result must equal the
+"""Row-sharded driver (paper_2104_00303_b200/sharded.py) at world sizes 2 and
+4 on CPU (gloo), with the numpy shard backend: the sharded result must equal the
 single-process exact-arithmetic model bit for bit (labels in global
 first-appearance numbering, modes, movement trace, per-iteration tables)."""
 
@@ -52,13 +52,13 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("name", sorted(CASES))
-def test_sharded_world2_equals_exact_model(name):
+@pytest.mark.parametrize("name,world", [(n, 2) for n in sorted(CASES)] + [("cloud3d", 4)])
+def test_sharded_equals_exact_model(name, world):
     gen, h, eta, mi = CASES[name]
     y = gen()
     with tempfile.TemporaryDirectory() as out:
-        mp.spawn(_worker, args=(2, _free_port(), y, h, eta, mi, out), nprocs=2, join=True)
-        parts = [dict(np.load(Path(out) / f"r{r}.npz")) for r in range(2)]
+        mp.spawn(_worker, args=(world, _free_port(), y, h, eta, mi, out), nprocs=world, join=True)
+        parts = [dict(np.load(Path(out) / f"r{r}.npz")) for r in range(world)]
     ref = X.meanshiftpp(y, h, eta, mi)
     for p in parts:
         assert int(p["iters"]) == ref["iterations"]
