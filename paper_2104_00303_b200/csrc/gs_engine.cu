@@ -859,14 +859,15 @@ __attribute__((target("avx512f"))) void expand_avx512(const u32* c0, const u32* 
 #endif
 
 // labels[i] = lab[c0[i]] over host threads
-void expand_labels(const u32* c0, const u32* lab, int64_t n, int64_t* out) {
+void expand_labels(const u32* c0, const u32* lab, int64_t n0, int64_t n, int64_t* out) {
   unsigned T = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  if (n < (int64_t)1 << 20) T = 1;
+  if (n - n0 < (int64_t)1 << 20) T = 1;
 #if defined(__x86_64__)
   const bool avx = __builtin_cpu_supports("avx512f");
 #endif
   auto work = [&](unsigned t) {
-    const int64_t a = (n * t / T) & ~int64_t(7), b = t + 1 == T ? n : (n * (t + 1) / T) & ~int64_t(7);
+    const int64_t m = n - n0;
+    const int64_t a = n0 + ((m * t / T) & ~int64_t(7)), b = t + 1 == T ? n : n0 + ((m * (t + 1) / T) & ~int64_t(7));
 #if defined(__x86_64__)
     if (avx) { expand_avx512(c0, lab, a, b, out); return; }
 #endif
@@ -880,6 +881,7 @@ void expand_labels(const u32* c0, const u32* lab, int64_t n, int64_t* out) {
 
 // the end of a host entry point: labels into the caller's host buffer
 void deliver_labels(gs_ctx* c, const int64_t* dl, int64_t* out, int64_t n) {
+  int64_t dev_bytes = 0;
   if (c->labels_on_host) {
     static const bool dbg = getenv("GS_DEBUG_DELIVERY") != nullptr;
     auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
@@ -887,8 +889,28 @@ void deliver_labels(gs_ctx* c, const int64_t* dl, int64_t* out, int64_t n) {
     GS_CUDA(cudaEventSynchronize(c->ev_cell0));
     sync(c);
     const double t1 = now();
-    expand_labels(c->h_cell0, c->h_slotlab, n, out);
-    c->xfer_d2h = (int64_t)sizeof(u32) * n + (int64_t)c->slotlab_bytes;
+    // a pinned caller buffer takes the first part of the labels straight from
+    // the device (int64, DMA) while the host threads expand the rest from the
+    // per-cell labels: the two run side by side
+    int64_t n_dev = 0;
+    cudaPointerAttributes pa;
+    if (n >= (int64_t)1 << 24 && cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
+        pa.type == cudaMemoryTypeHost && c->cell0_dev) {
+      n_dev = (n * 2 / 5) & ~int64_t(127);
+      int64_t* tmp = ensure<int64_t>(c, c->labels, (size_t)n);
+      launch(c, K_LABELS, [&] {
+        k_labels_from_slots<<<blocks_for(c, n_dev), kThreads, 0, c->st>>>(c->cell0_dev, n_dev,
+                                                                         static_cast<const u32*>(c->slotlab.p),
+                                                                         reinterpret_cast<i64*>(tmp));
+      });
+      GS_CUDA(cudaMemcpyAsync(out, tmp, sizeof(int64_t) * n_dev, cudaMemcpyDeviceToHost, c->st));
+    } else {
+      cudaGetLastError();   // (an unregistered pointer is not an error here)
+    }
+    expand_labels(c->h_cell0, c->h_slotlab, n_dev, n, out);
+    if (n_dev) sync(c);
+    dev_bytes = (int64_t)sizeof(int64_t) * n_dev;
+    c->xfer_d2h = (int64_t)sizeof(u32) * n + (int64_t)c->slotlab_bytes + dev_bytes;
     if (dbg) fprintf(stderr, "deliver: wait %.3f ms expand %.3f ms\n", t1 - t0, now() - t1);
   } else {
     GS_CUDA(cudaMemcpyAsync(out, dl, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));

@@ -1988,6 +1988,17 @@ __global__ void __launch_bounds__(kThreads) k_label_colors(const unsigned char* 
   }
 }
 
+// labels of the first n points from the per-cell labels (host delivery: this
+// part is copied to a pinned caller buffer while host threads expand the rest)
+__global__ void __launch_bounds__(kThreads) k_labels_from_slots(const u32* __restrict__ cell0, i64 n,
+                                                                const u32* __restrict__ slotlab, i64* labels) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 c = cell0[i];
+    labels[i] = c == 0xffffffffu ? -1 : (i64)slotlab[c];
+  }
+}
+
 // labels in original order: one coalesced pass (cell0 -> run root -> rank)
 __global__ void __launch_bounds__(kThreads) k_labels_runs(const u32* __restrict__ cell0, i64 n,
                                                           const u32* __restrict__ runroot,
