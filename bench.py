@@ -711,7 +711,8 @@ def e2e(x_host, cfg, n, steps):
     return {"value": ups / dt, "unit": UNIT, "h2d_bytes_per_step": int(hb.value),
             "d2h_bytes_per_step": int(db.value), "steps": steps,
             "labels": "int64 into the caller's pinned buffer; the sorted dense path sends 4 B/point of "
-                      "initial-cell index during the loop + 4 B/cell of labels and expands on the host",
+                      "initial-cell index during the loop + 4 B/cell of labels; host threads expand 60% of the "
+                      "labels from them while the device writes the other 40% into the pinned buffer by DMA",
             "api": "paper_2104_00303_b200.meanshiftpp_points(float32 (n,3), ShiftConfig) -> "
                    "gs_meanshiftpp_host (C ABI)"}
 
