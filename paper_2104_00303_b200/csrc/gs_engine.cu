@@ -756,9 +756,22 @@ void rs_next(gs_ctx* c, const Plan& p, Tab* tabs, int t, const Rec<D>* rec) {
 
 // Histogram of y[0] into table 0 (clean), before the loop.
 template <int D, class Tab>
-void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_pts, bool grouped = false) {
+void enqueue_first_hist(gs_ctx* c, const Plan& p, Tab* tabs, int64_t n, int nb_pts, bool grouped = false,
+                        const SortInfo* runs = nullptr) {
   Ctrl* ctrl = static_cast<Ctrl*>(c->ctrl.p);
   const double* y0 = static_cast<const double*>(c->y[0].p);
+  if constexpr (!Tab::kDense) {
+    // sorted hash-table runs: one plain-store entry per run of the spatial
+    // sort (measured against the per-tile CAS / atomic build: DESIGN.md 3)
+    static const bool off = getenv("GRIDSHIFT_HIST_RUNS") && getenv("GRIDSHIFT_HIST_RUNS")[0] == '0';
+    if (runs && grouped && !off) {
+      launch(c, K_HIST, [&] {
+        k_hist_runs<D, Tab><<<blocks_for(c, (int64_t)p.list_cap * kHistRunLanes), kThreads, 0, c->st>>>(
+            y0, p.g, tabs[0], runs->runs, &ctrl->nruns, runs->start, runs->end, ctrl);
+      });
+      return;
+    }
+  }
   // grouped: y0 is the spatial sort's output (each cell's points contiguous)
   if (grouped)
     launch(c, K_HIST, [&] { k_hist<D, Tab, false, true, true><<<nb_pts, kThreads, 0, c->st>>>(y0, n, p.g, tabs[0], ctrl, 0); });
@@ -1368,7 +1381,7 @@ RunOut run_engine_d(gs_ctx* c, const Input& in, int64_t n, double h, double eta,
   else if (p.dense)
     enqueue_first_hist<D>(c, p, tabs.dn, n, nb_pts, sorted);
   else
-    enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts, sorted);
+    enqueue_first_hist<D>(c, p, tabs.hs, n, nb_pts, sorted, sorted ? &sinfo : nullptr);
   // reference-order sums (default): the first table's sums in np.bincount
   // order, from the input values in original point order
   if (!c->exact_sums) {

@@ -1238,6 +1238,81 @@ struct BrickMap {
   }
 };
 
+// First table of a sorted hash-table run, from the runs of the spatial sort:
+// a run is one cell's points, contiguous in the sorted iterate, so a warp sums
+// it (exact fixed point; 8 lanes per run) and writes its entry with plain stores after one
+// insert -- no per-segment atomics (k_hist's hash path pays a CAS plus
+// 2 d + 1 atomic adds per cell segment of a tile).
+constexpr int kHistRunLanes = 8;   // lanes per run (a 4K RGB+xy image: ~14 points per run)
+
+template <int D, class Tab>
+__global__ void __launch_bounds__(kThreads) k_hist_runs(const double* __restrict__ y, GridParams g, Tab tab,
+                                                        const u32* __restrict__ runs, const u32* nruns,
+                                                        const u32* __restrict__ start,
+                                                        const u32* __restrict__ end, Ctrl* ctrl) {
+  constexpr int G = kHistRunLanes;
+  const u32 R = *nruns;
+  const int sub = threadIdx.x & (G - 1);
+  const i64 gg = ((i64)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const i64 ng = ((i64)gridDim.x * blockDim.x) / G;
+  // (whole warps stay in the loop: the shuffles below are warp-wide)
+  const i64 rounds = ((i64)R + ng - 1) / ng;
+  for (i64 it = 0; it < rounds; ++it) {
+    const i64 a = gg + it * ng;
+    const bool live = a < (i64)R;
+    const u32 r = live ? runs[a] : 0u;
+    const u32 p0 = live ? start[r] : 0u, p1 = live ? end[r] : 0u;
+    Agg<D> ag;
+    ag.zero();
+    for (u32 p = p0 + sub; p < p1; p += G) {
+      ag.cnt += 1;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const i64 f = to_fixed(y[(i64)j * g.ld + p], g.qscale[j]);
+        ag.hi[j] += f >> 32;
+        ag.lo[j] += (u64)(f & 0xffffffffll);
+      }
+    }
+#pragma unroll
+    for (int off = G / 2; off; off >>= 1) {   // sum over the run's lane group
+      ag.cnt += __shfl_xor_sync(kFull, ag.cnt, off);
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        ag.hi[j] += (i64)__shfl_xor_sync(kFull, (unsigned long long)ag.hi[j], off);
+        ag.lo[j] += __shfl_xor_sync(kFull, ag.lo[j], off);
+      }
+    }
+    if (sub == 0 && p1 > p0) {
+      double v[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = y[(i64)j * g.ld + p0];
+      bool inside;
+      const u64 key = pack_key<D>(g, v, inside);
+      bool fresh;
+      const u32 s = tab.insert(key, fresh, &ctrl->error);
+      if (s != 0xffffffffu) {
+        if (fresh) tab.list[atomicAdd(tab.k, 1u)] = s;
+        Entry<D>* e = tab.ent + s;
+        if (fresh) {               // (always: the runs are distinct cells)
+          e->count = ag.cnt;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            e->hi[j] = (u64)ag.hi[j];
+            e->lo[j] = ag.lo[j];
+          }
+        } else {
+          atomicAdd(&e->count, (u64)ag.cnt);
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            atomicAdd(&e->hi[j], (u64)ag.hi[j]);
+            atomicAdd(&e->lo[j], ag.lo[j]);
+          }
+        }
+      }
+    }
+  }
+}
+
 // Brick occupancy of a freshly built table (the derived tables mark theirs
 // in k_derive_brick3); occ zeroed before.
 __global__ void __launch_bounds__(kThreads) k_mark_bricks(const Entry<3>* ent, u64 nslots, BrickMap bm, u8* occ) {
